@@ -1,0 +1,276 @@
+"""CPU ORACLE — test infrastructure only, never the product path.
+
+A plain NumPy/SciPy restatement of the reference's hot-path algorithms
+(/root/reference/pkg/src/specdens, cited per function).  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline / reference legs
+may import it, and only as the checker or the timed CPU baseline.
+
+Pinning: ``tests/golden/make_golden.py`` runs the reference itself (importable
+in the build container) on fixed seeded inputs and stores its outputs under
+``tests/golden/``; ``tests/test_oracle_golden.py`` checks this module against
+those fixtures (bit-for-bit where the arithmetic order is the same).
+
+Third-party arithmetic the reference delegates to (pinned only as
+``numpy>=2.0, scipy>=1.13`` in pkg/pyproject.toml:9-12; this image has NumPy
+2.3.5, SciPy 1.18.1):
+  * SciPy ``csr_matvec`` (csr @ x): y_i = sum over the row's stored entries in
+    storage order -- used here through the same SciPy call;
+  * LAPACK ``?stevd`` via ``scipy.linalg.eigh_tridiagonal`` -- same call;
+  * NumPy Philox/SeedSequence probe streams -- same calls.
+"""
+
+import numpy as np
+import scipy.sparse as sp
+from scipy.linalg import eigh_tridiagonal
+
+EDGE_GUARD = 1e-6
+BREAKDOWN_RTOL = 1e-13
+
+
+class OracleNumericalFailure(RuntimeError):
+    pass
+
+
+# ---- probes: stochastic.py:40-54 -------------------------------------------------
+def draw_probe(kind, seed, dim, index, stream=0):
+    if kind == "basis":
+        v = np.zeros(dim)
+        v[index] = np.sqrt(dim)
+        return v
+    ss = np.random.SeedSequence(seed, spawn_key=(stream, index))
+    rng = np.random.Generator(np.random.Philox(ss))
+    if kind == "gaussian":
+        return rng.standard_normal(dim)
+    return rng.integers(0, 2, dim) * 2.0 - 1.0
+
+
+def as_csr(matrix):
+    if sp.issparse(matrix):
+        return sp.csr_array(matrix)
+    if hasattr(matrix, "csr"):
+        return matrix.csr
+    return sp.csr_array(np.asarray(matrix, dtype=float))
+
+
+# ---- mapped matvec: matrix.py:101-102, :125-126 -------------------------------------
+def mapped_matvec(csr, c, d, x):
+    return (csr @ x - c * x) / d
+
+
+# ---- kpm.py:96-107 --------------------------------------------------------------------
+def chebyshev_probe_moments(csr, c, d, degree, v0):
+    zeta = np.empty(degree + 1)
+    zeta[0] = v0 @ v0
+    if degree == 0:
+        return zeta
+    v_prev = v0
+    v_cur = mapped_matvec(csr, c, d, v0)
+    zeta[1] = v0 @ v_cur
+    for k in range(2, degree + 1):
+        v_cur, v_prev = 2.0 * mapped_matvec(csr, c, d, v_cur) - v_prev, v_cur
+        zeta[k] = v0 @ v_cur
+    return zeta
+
+
+# ---- kpm.py:174-189 (product formula, one probe) ------------------------------------------
+def product_formula_probe_moments(csr, c, d, degree, v0):
+    p = (degree + 1) // 2
+    stored = np.empty((p + 1, len(v0)))
+    stored[0] = v0
+    if p >= 1:
+        stored[1] = mapped_matvec(csr, c, d, stored[0])
+    for j in range(2, p + 1):
+        stored[j] = 2.0 * mapped_matvec(csr, c, d, stored[j - 1]) - stored[j - 2]
+    zeta = np.empty(degree + 1)
+    for k in range(0, p + 1):
+        if k <= degree:
+            zeta[k] = v0 @ stored[k]
+    for k in range(p + 1, degree + 1):
+        a = (k + 1) // 2
+        b = k - a
+        zeta[k] = 2.0 * (stored[a] @ stored[b]) - zeta[a - b]
+    return zeta
+
+
+# ---- doubling identities of the north star (the form the GPU kernel computes) ----------------
+def doubling_probe_moments(csr, c, d, degree, v0):
+    """zeta_{2k} = 2<w_k,w_k> - zeta_0, zeta_{2k+1} = 2<w_{k+1},w_k> - zeta_1 (kpm.py:162-163)."""
+    zeta = np.empty(degree + 1)
+    zeta[0] = v0 @ v0
+    if degree == 0:
+        return zeta
+    w_prev, w = None, v0
+    k = 0
+    while True:
+        w_next = mapped_matvec(csr, c, d, w) if k == 0 else 2.0 * mapped_matvec(csr, c, d, w) - w_prev
+        if 2 * k + 1 <= degree:
+            r = w_next @ w
+            zeta[2 * k + 1] = r if k == 0 else 2.0 * r - zeta[1]
+        if 2 * k + 2 <= degree:
+            zeta[2 * k + 2] = 2.0 * (w_next @ w_next) - zeta[0]
+        k += 1
+        if 2 * k + 1 > degree:
+            break
+        w_prev, w = w, w_next
+    return zeta
+
+
+# ---- kpm.py:127-140 ----------------------------------------------------------------------
+def average_moments(per_probe):
+    zeta = np.mean(np.asarray(per_probe), axis=0)
+    if not np.all(np.isfinite(zeta)):
+        raise OracleNumericalFailure("non-finite moments")
+    return zeta
+
+
+def chebyshev_moments(matrix, c, d, degree, kind, seed, n_vec, mode="direct", stream=0, indices=None):
+    """Per-probe moments (n_vec x (degree+1)) over probe indices 0..n_vec-1."""
+    csr = as_csr(matrix)
+    n = csr.shape[0]
+    fn = {"direct": chebyshev_probe_moments, "product": product_formula_probe_moments,
+          "doubling": doubling_probe_moments}[mode]
+    idx = range(n_vec) if indices is None else indices
+    return np.array([fn(csr, c, d, degree, draw_probe(kind, seed, n, l, stream)) for l in idx])
+
+
+# ---- kpm.py:84-93, :201-217, :234-250 ------------------------------------------------------
+def jackson_damping(degree):
+    k = np.arange(degree + 1)
+    a = np.pi / (degree + 2)
+    return ((1.0 - k / (degree + 2)) * np.sin(a) * np.cos(k * a)
+            + np.sin(k * a) * np.cos(a) / (degree + 2)) / np.sin(a)
+
+
+def moments_to_coefficients(zeta, n, damping="none"):
+    degree = len(zeta) - 1
+    g = np.ones(degree + 1) if damping == "none" else jackson_damping(degree)
+    prefactor = np.full(degree + 1, 2.0 / (n * np.pi))
+    prefactor[0] = 1.0 / (n * np.pi)
+    return prefactor * zeta * g
+
+
+def evaluate_chebyshev_series(coeffs, t):
+    b1 = np.zeros_like(t)
+    b2 = np.zeros_like(t)
+    for c in coeffs[:0:-1]:
+        b1, b2 = 2.0 * t * b1 - b2 + c, b1
+    return t * b1 - b2 + coeffs[0]
+
+
+def unit_grid(n_pts):
+    h = 2.0 / n_pts
+    return -1.0 + (np.arange(n_pts) + 0.5) * h
+
+
+def interval_grid(lb, ub, n_pts, pad=0.0):
+    lo, hi = lb - pad, ub + pad
+    h = (hi - lo) / n_pts
+    return lo + (np.arange(n_pts) + 0.5) * h
+
+
+def evaluate_kpm_dos(coeffs, d, t):
+    """(values, density) on unit points t (kpm.py:244-250, density.py:124-136)."""
+    if np.any(np.abs(t) > 1.0 - EDGE_GUARD):
+        raise ValueError("grid point too close to the interval edge")
+    values = evaluate_chebyshev_series(coeffs, t) / np.sqrt(1.0 - t * t)
+    return values, values / d
+
+
+# ---- lanczos.py:67-131 ---------------------------------------------------------------------
+def lanczos_factorize(csr, v0, steps, reorth="full", c=0.0, d=1.0):
+    """Returns (alpha, beta, beta_next, basis, breakdown)."""
+    def matvec(x):
+        y = csr @ x
+        return y if (c == 0.0 and d == 1.0) else (y - c * x) / d
+
+    v0 = np.asarray(v0, dtype=float)
+    nrm = np.linalg.norm(v0)
+    if nrm == 0.0:
+        raise ValueError("starting vector must be nonzero")
+    dim = csr.shape[0]
+    basis = np.empty((dim, steps))
+    basis[:, 0] = v0 / nrm
+    alpha = np.empty(steps)
+    beta = np.empty(max(steps - 1, 0))
+    sqrt_eps = np.sqrt(np.finfo(float).eps)
+    beta_next = 0.0
+    tscale = 0.0
+    for j in range(steps):
+        w = matvec(basis[:, j])
+        if j > 0:
+            w = w - beta[j - 1] * basis[:, j - 1]
+        a = float(basis[:, j] @ w)
+        w -= a * basis[:, j]
+        alpha[j] = a
+        if reorth == "full":
+            for _ in range(2):
+                w -= basis[:, : j + 1] @ (basis[:, : j + 1].T @ w)
+        elif reorth == "selective":
+            overlaps = basis[:, : j + 1].T @ w
+            big = np.abs(overlaps) > sqrt_eps * np.linalg.norm(w)
+            if big.any():
+                w -= basis[:, : j + 1][:, big] @ overlaps[big]
+        b = float(np.linalg.norm(w))
+        if not (np.isfinite(a) and np.isfinite(b)):
+            raise OracleNumericalFailure(f"non-finite Lanczos recurrence at step {j + 1}")
+        tscale = max(tscale, abs(a), b)
+        if j == steps - 1:
+            beta_next = b
+        elif b <= BREAKDOWN_RTOL * max(tscale, 1.0):
+            return alpha[: j + 1], beta[:j], 0.0, basis[:, : j + 1], True
+        else:
+            beta[j] = b
+            basis[:, j + 1] = w / b
+    return alpha, beta, beta_next, basis, False
+
+
+# ---- lanczos.py:152-159, :170-187 ---------------------------------------------------------------
+def ritz_quadrature(alpha, beta):
+    if len(alpha) == 1:
+        return alpha.copy(), np.ones(1)
+    theta, y = eigh_tridiagonal(alpha, beta)
+    return theta, y[0, :] ** 2
+
+
+def pool(quads):
+    theta = np.concatenate([q[0] for q in quads])
+    tau = np.concatenate([q[1] for q in quads]) / len(quads)
+    order = np.argsort(theta)
+    return theta[order], tau[order]
+
+
+def gaussian(x, sigma):
+    return np.exp(-0.5 * (x / sigma) ** 2) / np.sqrt(2.0 * np.pi * sigma * sigma)
+
+
+def blur_nodes(theta, weights, grid, sigma, block=512):
+    out = np.zeros_like(grid, dtype=float)
+    for start in range(0, len(theta), block):
+        th = theta[start:start + block]
+        wt = weights[start:start + block]
+        out += gaussian(grid[None, :] - th[:, None], sigma).T @ wt
+    return out
+
+
+def lanczos_dos(matrix, steps, kind, seed, n_vec, sigma, grid, reorth="full", indices=None):
+    """(density, nodes, weights, per-probe (alpha, beta, beta_next))."""
+    csr = as_csr(matrix)
+    n = csr.shape[0]
+    idx = range(n_vec) if indices is None else indices
+    quads, facts = [], []
+    for l in idx:
+        a, b, bn, _, _ = lanczos_factorize(csr, draw_probe(kind, seed, n, l), steps, reorth)
+        facts.append((a, b, bn))
+        quads.append(ritz_quadrature(a, b))
+    theta, tau = pool(quads)
+    return blur_nodes(theta, tau, grid, sigma), theta, tau, facts
+
+
+# ---- Gershgorin (configs) ---------------------------------------------------------------------
+def gershgorin(csr):
+    n = csr.shape[0]
+    rows = np.repeat(np.arange(n), np.diff(csr.indptr))
+    on = rows == csr.indices
+    dg = np.bincount(rows[on], weights=csr.data[on], minlength=n)
+    rad = np.bincount(rows[~on], weights=np.abs(csr.data[~on]), minlength=n)
+    return float(np.min(dg - rad)), float(np.max(dg + rad))

@@ -1,0 +1,102 @@
+// common.cuh — shared plumbing for the specdens_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "../../include/specdens_b200.h"
+
+namespace sdb {
+
+// ---- error reporting (thread-local message, status codes) ----------------
+void set_error(const std::string& msg);
+int fail(int code, const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+
+#define SDB_CUDA(call)                                                         \
+  do {                                                                         \
+    cudaError_t _e = (call);                                                   \
+    if (_e != cudaSuccess) return ::sdb::cuda_fail(_e, #call, __FILE__, __LINE__); \
+  } while (0)
+
+#define SDB_CHECK_LAUNCH() SDB_CUDA(cudaGetLastError())
+
+#define SDB_REQUIRE(cond, ...)                                                 \
+  do {                                                                         \
+    if (!(cond)) return ::sdb::fail(SDB_EINVAL, __VA_ARGS__);                 \
+  } while (0)
+
+// Switch the calling thread to `device` for the lifetime of the guard.
+struct DeviceGuard {
+  int prev = -1;
+  int ok = 0;
+  explicit DeviceGuard(int device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = (cudaSetDevice(device) == cudaSuccess);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int num_sms(int device);
+
+// ---- matrix handle ---------------------------------------------------------
+struct StencilDev {
+  int64_t nx, ny, nz;
+  int32_t n_off;
+  int32_t off[26][3];
+  double w[26];
+};
+
+}  // namespace sdb
+
+struct sdb_matrix {
+  int device = 0;
+  int format = SDB_FMT_CSR;
+  int64_t n = 0;
+  int64_t nnz = 0;
+  // CSR (int32 row pointers and column indices: nnz < 2^31)
+  int32_t* rowptr = nullptr;
+  int32_t* colidx = nullptr;
+  double* values = nullptr;
+  // stencil
+  sdb::StencilDev st{};
+  double* diag = nullptr;
+};
+
+namespace sdb {
+
+// Blocks of the persistent row-range kernels.  Depends on n and the SM count
+// only, so the reduction tree (and hence every bit of the result) is fixed for
+// a given matrix on a given GPU model.
+int64_t row_blocks(const sdb_matrix* m);
+
+// Row group geometry: L lanes per row (power of two <= 32), each lane holding
+// VPL double2 values; ldv = 2 * L * VPL.
+struct Geometry {
+  int L;
+  int VPL;
+  int64_t ldv;
+};
+Geometry choose_geometry(int64_t n_vec);
+
+// ---- device helpers ---------------------------------------------------------
+__device__ __forceinline__ double2 ld_d2(const double* p) {
+  return __ldg(reinterpret_cast<const double2*>(p));
+}
+// Streaming load of data touched once per pass (do not keep in L1).
+__device__ __forceinline__ double2 ld_d2_stream(const double* p) {
+  double2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_d2(double* p, double2 v) {
+  *reinterpret_cast<double2*>(p) = v;
+}
+
+}  // namespace sdb

@@ -1,0 +1,358 @@
+// dos.cu — K3 (Jackson damping, coefficients, Clenshaw DOS) and the Lanczos
+// quadrature back end: K6 batched tridiagonal eigensolver (first-row QL),
+// node pooling, and K7 Gaussian blur.
+#include <vector>
+
+#include "common.cuh"
+
+namespace sdb {
+
+// ---- K3 -----------------------------------------------------------------------
+// jackson_damping (kpm.py:84-93):
+//   g_k = [(1 - k/(M+2)) sin(a) cos(k a) + sin(k a) cos(a)/(M+2)] / sin(a),  a = pi/(M+2)
+__global__ void jackson_kernel(int64_t degree, double* __restrict__ g) {
+  const double mp2 = (double)(degree + 2);
+  const double a = M_PI / mp2;
+  const double sa = sin(a), ca = cos(a);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= degree; k += (int64_t)gridDim.x * blockDim.x) {
+    const double kd = (double)k;
+    g[k] = ((1.0 - kd / mp2) * sa * cos(kd * a) + sin(kd * a) * ca / mp2) / sa;
+  }
+}
+
+// moments_to_coefficients (kpm.py:201-208): mu_k = prefactor_k * zeta_k * g_k,
+// prefactor = 2/(n pi) for k >= 1 and 1/(n pi) for k = 0.
+__global__ void coefficients_kernel(const double* __restrict__ zeta, int64_t degree, int64_t n, int damping,
+                                    double* __restrict__ mu) {
+  const double npi = (double)n * M_PI;
+  const double mp2 = (double)(degree + 2);
+  const double a = M_PI / mp2;
+  const double sa = sin(a), ca = cos(a);
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k <= degree; k += (int64_t)gridDim.x * blockDim.x) {
+    const double pref = (k == 0 ? 1.0 : 2.0) / npi;
+    double g = 1.0;
+    if (damping == SDB_DAMP_JACKSON) {
+      const double kd = (double)k;
+      g = ((1.0 - kd / mp2) * sa * cos(kd * a) + sin(kd * a) * ca / mp2) / sa;
+    }
+    mu[k] = pref * zeta[k] * g;
+  }
+}
+
+// evaluate_chebyshev_series (kpm.py:211-217) by Clenshaw, one grid point per
+// thread, coefficients staged through shared memory in tiles; then the
+// Chebyshev weight 1/sqrt(1-t^2) (kpm.py:247) and the 1/d unmapping
+// (density.py:124-136).
+__global__ void series_kernel(const double* __restrict__ mu, int64_t degree, const double* __restrict__ t,
+                              int64_t n_pts, int edge_weight, double divisor, double* __restrict__ values,
+                              double* __restrict__ density) {
+  constexpr int TILE = 1024;
+  __shared__ double cs[TILE];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = i < n_pts;
+  const double ti = live ? t[i] : 0.0;
+  const double t2 = 2.0 * ti;
+  double b1 = 0.0, b2 = 0.0;
+  // coefficients M..1, walked downwards in tiles of TILE
+  for (int64_t hi = degree; hi >= 1; hi -= TILE) {
+    const int64_t lo = hi - TILE + 1 < 1 ? 1 : hi - TILE + 1;
+    __syncthreads();
+    for (int64_t k = lo + threadIdx.x; k <= hi; k += blockDim.x) cs[k - lo] = mu[k];
+    __syncthreads();
+    for (int64_t k = hi; k >= lo; --k) {
+      const double nb1 = t2 * b1 - b2 + cs[k - lo];
+      b2 = b1;
+      b1 = nb1;
+    }
+  }
+  if (!live) return;
+  double v = ti * b1 - b2 + mu[0];
+  if (edge_weight) v = v / sqrt(1.0 - ti * ti);
+  values[i] = v;
+  if (density) density[i] = v / divisor;
+}
+
+// ---- K6: batched first-row implicit QL ---------------------------------------------
+// ritz_quadrature (lanczos.py:152-159) takes theta, y = eigh_tridiagonal(alpha,
+// beta) and tau^2 = y[0,:]^2.  Only the first row of the eigenvector matrix is
+// needed (Golub-Welsch), so the implicit-shift QL sweep applies each plane
+// rotation to a single row vector z (initialised to e_0) instead of a matrix.
+// One block per probe; the serial sweep runs on one thread with d, e, z in
+// shared memory.
+__global__ void ritz_ql_kernel(const double* __restrict__ alpha, const double* __restrict__ beta,
+                               const int32_t* __restrict__ steps_done, int64_t m, double* __restrict__ theta,
+                               double* __restrict__ tau2, int* failed) {
+  extern __shared__ double sh[];
+  double* d = sh;
+  double* e = sh + m;
+  double* z = sh + 2 * m;
+  const int64_t l = blockIdx.x;
+  const int64_t mm = steps_done[l];
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    d[i] = i < mm ? alpha[l * m + i] : 0.0;
+    e[i] = (i + 1 < mm) ? beta[l * m + i] : 0.0;
+    z[i] = (i == 0) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int64_t nn = mm;
+    for (int64_t lo = 0; lo < nn; ++lo) {
+      int iter = 0;
+      int64_t hi;
+      do {
+        // find the first negligible off-diagonal at or after lo
+        for (hi = lo; hi < nn - 1; ++hi) {
+          const double dd = fabs(d[hi]) + fabs(d[hi + 1]);
+          if (fabs(e[hi]) <= 2.220446049250313e-16 * dd) break;
+        }
+        if (hi != lo) {
+          if (++iter > 60) {
+            atomicExch(failed, 1);
+            break;
+          }
+          // Wilkinson-type shift from the leading 2x2 block
+          double g = (d[lo + 1] - d[lo]) / (2.0 * e[lo]);
+          double r = hypot(g, 1.0);
+          g = d[hi] - d[lo] + e[lo] / (g + copysign(r, g));
+          double s = 1.0, c = 1.0, p = 0.0;
+          int64_t i;
+          bool deflated = false;
+          for (i = hi - 1; i >= lo; --i) {
+            double f = s * e[i];
+            const double b = c * e[i];
+            r = hypot(f, g);
+            e[i + 1] = r;
+            if (r == 0.0) {  // underflow: split the problem here
+              d[i + 1] -= p;
+              e[hi] = 0.0;
+              deflated = true;
+              break;
+            }
+            s = f / r;
+            c = g / r;
+            g = d[i + 1] - p;
+            r = (d[i] - g) * s + 2.0 * c * b;
+            p = s * r;
+            d[i + 1] = g + p;
+            g = c * r - b;
+            // rotate columns i, i+1 of the (first row of the) eigenvector matrix
+            f = z[i + 1];
+            z[i + 1] = s * z[i] + c * f;
+            z[i] = c * z[i] - s * f;
+          }
+          if (deflated) continue;
+          d[lo] -= p;
+          e[lo] = g;
+          e[hi] = 0.0;
+        }
+      } while (hi != lo);
+    }
+    // ascending order (LAPACK convention), insertion sort carrying z
+    for (int64_t i = 1; i < nn; ++i) {
+      const double dv = d[i], zv = z[i];
+      int64_t j = i - 1;
+      while (j >= 0 && d[j] > dv) {
+        d[j + 1] = d[j];
+        z[j + 1] = z[j];
+        --j;
+      }
+      d[j + 1] = dv;
+      z[j + 1] = zv;
+    }
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    theta[l * m + i] = i < mm ? d[i] : 0.0;
+    tau2[l * m + i] = i < mm ? z[i] * z[i] : 0.0;
+  }
+}
+
+// ---- node pooling (lanczos.py:170-177) ---------------------------------------------
+// Stable rank sort of the concatenated nodes: rank(i) = #{j : th_j < th_i} +
+// #{j < i : th_j == th_i}.  O(N^2) compares on a tile of theta staged in
+// shared memory; N = probes x steps is small (12,800 at config 4).
+__global__ void compact_kernel(const double* __restrict__ theta, const double* __restrict__ tau2,
+                               const int64_t* __restrict__ offsets, const int32_t* __restrict__ steps_done,
+                               int64_t n_rows, int64_t m, double* __restrict__ flat_th, double* __restrict__ flat_w) {
+  const int64_t total = n_rows * m;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = idx / m, k = idx % m;
+    if (k >= steps_done[l]) continue;
+    flat_th[offsets[l] + k] = theta[idx];
+    flat_w[offsets[l] + k] = tau2[idx];
+  }
+}
+
+__global__ void rank_sort_kernel(const double* __restrict__ th, const double* __restrict__ w, int64_t count,
+                                 double divisor, double* __restrict__ nodes, double* __restrict__ weights) {
+  constexpr int TILE = 1024;
+  __shared__ double tile[TILE];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const double x = i < count ? th[i] : 0.0;
+  int64_t rank = 0;
+  for (int64_t t0 = 0; t0 < count; t0 += TILE) {
+    __syncthreads();
+    for (int64_t k = threadIdx.x; k < TILE && t0 + k < count; k += blockDim.x) tile[k] = th[t0 + k];
+    __syncthreads();
+    const int64_t lim = (count - t0) < TILE ? (count - t0) : TILE;
+    for (int64_t k = 0; k < lim; ++k) {
+      const double y = tile[k];
+      rank += (y < x) || (y == x && t0 + k < i);
+    }
+  }
+  if (i < count) {
+    nodes[rank] = x;
+    weights[rank] = w[i] / divisor;
+  }
+}
+
+// ---- K7: blur (lanczos.py:180-187, density.py:58-76) ---------------------------------
+// One block per grid point; threads stride over the nodes, then a fixed-order
+// shared-memory tree reduce (deterministic).
+__global__ void blur_kernel(const double* __restrict__ theta, const double* __restrict__ w, int64_t count,
+                            double scale, int kind, double width, const double* __restrict__ grid, int64_t n_pts,
+                            double* __restrict__ density) {
+  __shared__ double red[256];
+  const double gnorm = sqrt(2.0 * M_PI * width * width);
+  const double lnum = width / M_PI, w2 = width * width;
+  for (int64_t gi = blockIdx.x; gi < n_pts; gi += gridDim.x) {
+    const double x = grid[gi];
+    double s = 0.0;
+    for (int64_t k = threadIdx.x; k < count; k += blockDim.x) {
+      const double dx = x - theta[k];
+      double kv;
+      if (kind == SDB_KERNEL_GAUSSIAN) {
+        const double u = dx / width;
+        kv = exp(-0.5 * (u * u)) / gnorm;
+      } else {
+        kv = lnum / (dx * dx + w2);
+      }
+      s += kv * w[k];
+    }
+    red[threadIdx.x] = s;
+    __syncthreads();
+    for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+      if ((int)threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) density[gi] = scale * red[0];
+    __syncthreads();
+  }
+}
+
+}  // namespace sdb
+
+using namespace sdb;
+
+extern "C" {
+
+int sdb_jackson_damping(int64_t degree, double* g, void* stream) {
+  SDB_REQUIRE(g != nullptr, "NULL argument");
+  SDB_REQUIRE(degree >= 0, "degree must be non-negative");
+  int blocks = (int)((degree + 256) / 256);
+  jackson_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(degree, g);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+int sdb_kpm_coefficients(const double* zeta, int64_t degree, int64_t n, int damping, double* mu, void* stream) {
+  SDB_REQUIRE(zeta && mu, "NULL argument");
+  SDB_REQUIRE(degree >= 0 && n >= 1, "bad degree or dimension");
+  SDB_REQUIRE(damping == SDB_DAMP_NONE || damping == SDB_DAMP_JACKSON, "unknown damping kind %d", damping);
+  int blocks = (int)((degree + 256) / 256);
+  coefficients_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(zeta, degree, n, damping, mu);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+int sdb_chebyshev_series(const double* mu, int64_t degree, const double* t, int64_t n_pts, int edge_weight,
+                         double divisor, double* values, double* density, void* stream) {
+  SDB_REQUIRE(mu && t && values, "NULL argument");
+  SDB_REQUIRE(degree >= 0, "degree must be non-negative");
+  if (n_pts <= 0) return SDB_OK;
+  SDB_REQUIRE(density == nullptr || divisor != 0.0, "divisor must be non-zero");
+  int blocks = (int)((n_pts + 127) / 128);
+  series_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(mu, degree, t, n_pts, edge_weight, divisor, values,
+                                                          density);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+int sdb_ritz_quadrature(const double* alpha, const double* beta, const int32_t* steps_done, int64_t n_vec,
+                        int64_t m, double* theta, double* tau2, void* stream) {
+  SDB_REQUIRE(alpha && beta && steps_done && theta && tau2, "NULL argument");
+  SDB_REQUIRE(n_vec >= 1 && m >= 1, "bad shape");
+  size_t shmem = sizeof(double) * 3 * (size_t)m;
+  SDB_REQUIRE(shmem <= 200 * 1024, "tridiagonal order %lld too large for the on-chip eigensolver", (long long)m);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (shmem > 48 * 1024) SDB_CUDA(cudaFuncSetAttribute(ritz_ql_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
+  int* failed = nullptr;
+  SDB_CUDA(cudaMallocAsync(&failed, sizeof(int), s));
+  SDB_CUDA(cudaMemsetAsync(failed, 0, sizeof(int), s));
+  ritz_ql_kernel<<<(unsigned)n_vec, 64, shmem, s>>>(alpha, beta, steps_done, m, theta, tau2, failed);
+  cudaError_t le = cudaGetLastError();
+  int hf = 0;
+  cudaError_t e = le;
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&hf, failed, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(failed, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "ritz_ql_kernel", __FILE__, __LINE__);
+  if (hf) return fail(SDB_ENUMERIC, "tridiagonal eigensolver did not converge");
+  return SDB_OK;
+}
+
+int sdb_pool_nodes(const double* theta, const double* tau2, const int32_t* steps_done, int64_t n_rows, int64_t m,
+                   double divisor, double* nodes, double* weights, int64_t* count, void* stream) {
+  SDB_REQUIRE(theta && tau2 && steps_done && nodes && weights && count, "NULL argument");
+  SDB_REQUIRE(n_rows >= 1 && m >= 1, "bad shape");
+  SDB_REQUIRE(divisor != 0.0, "divisor must be non-zero");
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<int32_t> sd((size_t)n_rows);
+  SDB_CUDA(cudaMemcpyAsync(sd.data(), steps_done, sizeof(int32_t) * n_rows, cudaMemcpyDeviceToHost, s));
+  SDB_CUDA(cudaStreamSynchronize(s));
+  std::vector<int64_t> off((size_t)n_rows);
+  int64_t total = 0;
+  for (int64_t l = 0; l < n_rows; ++l) {
+    SDB_REQUIRE(sd[l] >= 0 && sd[l] <= m, "steps_done out of range");
+    off[l] = total;
+    total += sd[l];
+  }
+  *count = total;
+  if (total == 0) return SDB_OK;
+  int64_t* d_off = nullptr;
+  double* flat = nullptr;
+  SDB_CUDA(cudaMallocAsync(&d_off, sizeof(int64_t) * n_rows, s));
+  SDB_CUDA(cudaMallocAsync(&flat, sizeof(double) * 2 * total, s));
+  SDB_CUDA(cudaMemcpyAsync(d_off, off.data(), sizeof(int64_t) * n_rows, cudaMemcpyHostToDevice, s));
+  int64_t work = n_rows * m;
+  compact_kernel<<<(int)((work + 255) / 256), 256, 0, s>>>(theta, tau2, d_off, steps_done, n_rows, m, flat,
+                                                           flat + total);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) {
+    rank_sort_kernel<<<(int)((total + 255) / 256), 256, 0, s>>>(flat, flat + total, total, divisor, nodes, weights);
+    e = cudaGetLastError();
+  }
+  cudaFreeAsync(d_off, s);
+  cudaFreeAsync(flat, s);
+  // the host offsets vector dies here: make sure the async upload finished
+  cudaError_t e2 = cudaStreamSynchronize(s);
+  if (e == cudaSuccess) e = e2;
+  if (e != cudaSuccess) return cuda_fail(e, "sdb_pool_nodes", __FILE__, __LINE__);
+  return SDB_OK;
+}
+
+int sdb_blur_nodes(const double* theta, const double* w, int64_t count, double scale, int kind, double width,
+                   const double* grid, int64_t n_pts, double* density, void* stream) {
+  SDB_REQUIRE(grid && density, "NULL argument");
+  SDB_REQUIRE(count == 0 || (theta && w), "NULL argument");
+  SDB_REQUIRE(kind == SDB_KERNEL_GAUSSIAN || kind == SDB_KERNEL_LORENTZIAN, "unknown kernel kind %d", kind);
+  SDB_REQUIRE(width > 0.0, "kernel width must be positive");
+  if (n_pts <= 0) return SDB_OK;
+  int blocks = (int)(n_pts < 65535 ? n_pts : 65535);
+  blur_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(theta, w, count, scale, kind, width, grid, n_pts, density);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,534 @@
+// lanczos.cu — batched lock-step Lanczos with full reorthogonalisation.
+//
+// Reference: lanczos_factorize (lanczos.py:67-131), one probe at a time:
+//   basis[:,0] = v0/||v0||
+//   for j: w = A v_j - beta_{j-1} v_{j-1};  alpha_j = v_j . w;  w -= alpha_j v_j
+//          full: 2x  w -= V (V^T w)          (classical Gram-Schmidt, twice)
+//          selective: h = V^T w; w -= V[:, |h| > sqrt(eps)||w||] h[...]
+//          beta_j = ||w||; non-finite -> NumericalFailure; breakdown if
+//          beta_j <= 1e-13 max(tscale, 1) -> truncate; v_{j+1} = w / beta_j
+// Here all probes of a batch run the same step together on an n x ldv block.
+// Each probe keeps its own basis V_l (the basis is stored step-major,
+// basis[t][i][l]), so the CGS projections are batched GEMVs, not a GEMM: no
+// operand is shared across probes, and the passes are HBM-bound.  Per step:
+//   K4  lz_spmm    w = A v_j - beta v_{j-1}, v_j = w_prev/beta written to the
+//                  basis on the fly, alpha partials
+//   K5a lz_proj    h = V_{0..j}^T w (one warp per basis vector t streaming its
+//                  rows; the first projection also applies w -= alpha v_j)
+//   K5b lz_update  w -= V_{0..j} h, optional ||w||^2 partials
+// and small fixed-order reduce kernels between them (deterministic).  A probe
+// that breaks down is frozen (1/beta = 0) while the others continue.
+#include <cmath>
+
+#include "rowgroup.cuh"
+
+namespace sdb {
+
+constexpr int kProjWarps = 8;
+
+struct LzState {       // per-probe device state, each an ldv-long array
+  double* inv_beta;    // 1/beta_{j-1} (0 once frozen)
+  double* beta_prev;   // beta_{j-1}
+  double* tscale;      // max |alpha|, beta seen so far (lanczos.py:114)
+  double* alpha_cur;   // alpha_j
+};
+
+// ---- start: ||v0|| --------------------------------------------------------------
+template <int L, int VPL>
+__global__ void __launch_bounds__(kRowThreads) lz_start_norm(const double* __restrict__ v0, int64_t n, int64_t ldv,
+                                                             int64_t nblocks, double* partials) {
+  constexpr int RPW = 32 / L, RPB = RPW * kRowWarps;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / L, q = lane % L;
+  const int64_t rs = n * blockIdx.x / nblocks, re = n * (blockIdx.x + 1) / nblocks;
+  double2 acc[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) acc[v] = make_double2(0.0, 0.0);
+  for (int64_t base = rs; base < re; base += RPB) {
+    const int64_t row = base + warp * RPW + g;
+    if (row < re) {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        double2 p = ld_d2(v0 + row * ldv + 2 * q + 2 * L * v);
+        acc[v].x += p.x * p.x;
+        acc[v].y += p.y * p.y;
+      }
+    }
+  }
+  __shared__ double smem[kRowWarps * SDB_MAX_BATCH];
+  block_partial<L, VPL>(acc, smem, partials, 0, nblocks, ldv);
+}
+
+__global__ void lz_start_reduce(const double* __restrict__ partials, int64_t nblocks, int64_t ldv, int64_t n_vec,
+                                LzState st, int32_t* __restrict__ steps_done, int32_t* __restrict__ status) {
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (l >= ldv) return;
+  const double nrm = sqrt(sum_blocks(partials, 0, nblocks, ldv, l));
+  const bool live = l < n_vec && nrm != 0.0 && isfinite(nrm);
+  st.inv_beta[l] = live ? 1.0 / nrm : 0.0;
+  st.beta_prev[l] = 0.0;
+  st.tscale[l] = 0.0;
+  st.alpha_cur[l] = 0.0;
+  if (l < n_vec) {
+    steps_done[l] = 0;
+    status[l] = (nrm == 0.0) ? SDB_LZ_ZERO_START : (isfinite(nrm) ? SDB_LZ_OK : SDB_LZ_NONFINITE);
+  }
+}
+
+// ---- K4: w = A v_j - beta_{j-1} v_{j-1}, v_j = w_prev * inv_beta, alpha partials ----
+template <class View, int L, int VPL>
+__global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
+    lz_spmm(View A, const double* __restrict__ wprev, const double* __restrict__ vprev, double* __restrict__ vj,
+            double* __restrict__ wout, LzState st, int first, double c, double inv_d, int64_t n, int64_t ldv,
+            int64_t nblocks, double* partials) {
+  constexpr int RPW = 32 / L, RPB = RPW * kRowWarps;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / L, q = lane % L;
+  const int64_t rs = n * blockIdx.x / nblocks, re = n * (blockIdx.x + 1) / nblocks;
+  double2 ib[VPL], bp[VPL], acc[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    ib[v] = ld_d2(st.inv_beta + 2 * q + 2 * L * v);
+    bp[v] = ld_d2(st.beta_prev + 2 * q + 2 * L * v);
+    acc[v] = make_double2(0.0, 0.0);
+  }
+  for (int64_t base = rs; base < re; base += RPB) {
+    const int64_t row = base + warp * RPW + g;
+    const bool valid = row < re;
+    double2 y[VPL];
+    spmv_row<L, VPL>(A, row, valid, valid ? (int)row : (int)rs, wprev, ldv, q, y);
+    if (valid) {
+      const int64_t o = row * ldv + 2 * q;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int off = 2 * L * v;
+        double2 wp = ld_d2(wprev + o + off);
+        double2 vv = make_double2(wp.x * ib[v].x, wp.y * ib[v].y);  // v_j = w / beta
+        st_d2(vj + o + off, vv);
+        // (A v_j - c v_j)/d  (the MappedOperator form, matrix.py:126)
+        double2 w = make_double2((y[v].x * ib[v].x - c * vv.x) * inv_d, (y[v].y * ib[v].y - c * vv.y) * inv_d);
+        if (!first) {
+          double2 pv = ld_d2(vprev + o + off);
+          w.x -= bp[v].x * pv.x;
+          w.y -= bp[v].y * pv.y;
+        }
+        st_d2(wout + o + off, w);
+        acc[v].x += vv.x * w.x;
+        acc[v].y += vv.y * w.y;
+      }
+    }
+  }
+  __shared__ double smem[kRowWarps * SDB_MAX_BATCH];
+  block_partial<L, VPL>(acc, smem, partials, 0, nblocks, ldv);
+}
+
+__global__ void lz_alpha_reduce(const double* __restrict__ partials, int64_t nblocks, int64_t ldv, int64_t n_vec,
+                                int64_t j, int64_t steps, LzState st, double* __restrict__ alpha,
+                                const int32_t* __restrict__ status) {
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (l >= ldv) return;
+  const double a = sum_blocks(partials, 0, nblocks, ldv, l);
+  const bool live = l < n_vec && status[l] == SDB_LZ_OK;
+  st.alpha_cur[l] = live ? a : 0.0;
+  if (live) alpha[l * steps + j] = a;
+}
+
+// ---- K5a: h[t] = V_t^T w for t <= j  (one warp per basis vector) ----------------
+// Block (t-chunk, row block).  Warp w handles t = chunk*8 + w and streams the
+// contiguous rows V[t][rs..re) of its row block; the w rows are shared by the
+// block's warps through L1.  When SUB_ALPHA, w' = w - alpha v_j is formed on
+// the fly and the warp handling t == 0 stores it to wdst (a different
+// buffer, so concurrent blocks never see a half-updated w).  NORM adds
+// ||w'||^2 partials (selective mode) at slot norm_slot.
+template <int NV, bool SUB_ALPHA, bool NORM>
+__global__ void __launch_bounds__(kProjWarps * 32)
+    lz_proj(const double* __restrict__ basis, const double* __restrict__ wsrc, double* __restrict__ wdst, LzState st,
+            int64_t j, int64_t n, int64_t ldv, int64_t nrb, double* partials, int64_t norm_slot) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t tchunk = blockIdx.x, rb = blockIdx.y;
+  const int64_t t = tchunk * kProjWarps + warp;
+  const int64_t rs = n * rb / nrb, re = n * (rb + 1) / nrb;
+  const size_t plane = (size_t)n * ldv;
+  const double* vt = basis + (size_t)t * plane;
+  const double* vj = basis + (size_t)j * plane;
+  double2 acc[NV], nacc[NV], al[NV];
+  bool colok[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    const int64_t col = 2 * (lane + 32 * v);
+    colok[v] = col < ldv;
+    acc[v] = nacc[v] = make_double2(0.0, 0.0);
+    al[v] = (SUB_ALPHA && colok[v]) ? ld_d2(st.alpha_cur + col) : make_double2(0.0, 0.0);
+  }
+  const bool active = t <= j;
+  const bool storer = SUB_ALPHA && tchunk == 0 && warp == 0;
+  if (active) {
+#pragma unroll 4
+    for (int64_t i = rs; i < re; ++i) {
+      const int64_t o = i * ldv + 2 * lane;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        if (!colok[v]) continue;
+        double2 w = ld_d2(wsrc + o + 64 * v);
+        if (SUB_ALPHA) {
+          double2 p = ld_d2(vj + o + 64 * v);
+          w.x -= al[v].x * p.x;
+          w.y -= al[v].y * p.y;
+          if (storer) st_d2(wdst + o + 64 * v, w);
+          if (NORM && storer) {
+            nacc[v].x += w.x * w.x;
+            nacc[v].y += w.y * w.y;
+          }
+        }
+        double2 b = ld_d2_stream(vt + o + 64 * v);
+        acc[v].x += b.x * w.x;
+        acc[v].y += b.y * w.y;
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!colok[v]) continue;
+      const int64_t col = 2 * (lane + 32 * v);
+      double* p = partials + ((size_t)t * nrb + rb) * ldv + col;
+      p[0] = acc[v].x;
+      p[1] = acc[v].y;
+    }
+  }
+  if (NORM && storer) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      if (!colok[v]) continue;
+      const int64_t col = 2 * (lane + 32 * v);
+      double* p = partials + ((size_t)norm_slot * nrb + rb) * ldv + col;
+      p[0] = nacc[v].x;
+      p[1] = nacc[v].y;
+    }
+  }
+}
+
+// h[t][l] = sum over row blocks (t <= j).  Selective mode keeps only the
+// overlaps above sqrt(eps) ||w|| (lanczos.py:107-110).
+__global__ void lz_h_reduce(const double* __restrict__ partials, int64_t nrb, int64_t ldv, int64_t j,
+                            double* __restrict__ h, int selective, int64_t norm_slot) {
+  const int64_t total = (j + 1) * ldv;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = idx / ldv, l = idx % ldv;
+    double v = sum_blocks(partials, t, nrb, ldv, l);
+    if (selective) {
+      const double wn = sqrt(sum_blocks(partials, norm_slot, nrb, ldv, l));
+      if (!(fabs(v) > 1.4901161193847656e-08 * wn)) v = 0.0;
+    }
+    h[idx] = v;
+  }
+}
+
+// ---- K5b: w -= V h (row-local), optional ||w||^2 partials ---------------------------
+template <int L, int VPL, bool NORM>
+__global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
+    lz_update(const double* __restrict__ basis, double* w, const double* __restrict__ h, int64_t j, int64_t n,
+              int64_t ldv, int64_t nblocks, double* partials) {
+  constexpr int RPW = 32 / L, RPB = RPW * kRowWarps;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / L, q = lane % L;
+  const int64_t rs = n * blockIdx.x / nblocks, re = n * (blockIdx.x + 1) / nblocks;
+  const size_t plane = (size_t)n * ldv;
+  double2 acc[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) acc[v] = make_double2(0.0, 0.0);
+  for (int64_t base = rs; base < re; base += RPB) {
+    const int64_t row = base + warp * RPW + g;
+    if (row < re) {
+      const int64_t o = row * ldv + 2 * q;
+      double2 s[VPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) s[v] = make_double2(0.0, 0.0);
+      int64_t t = 0;
+      for (; t + 4 <= j + 1; t += 4) {
+        double2 b[4][VPL], hh[4][VPL];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) {
+            b[u][v] = ld_d2_stream(basis + (size_t)(t + u) * plane + o + 2 * L * v);
+            hh[u][v] = ld_d2(h + (t + u) * ldv + 2 * q + 2 * L * v);
+          }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) {
+            s[v].x = fma(b[u][v].x, hh[u][v].x, s[v].x);
+            s[v].y = fma(b[u][v].y, hh[u][v].y, s[v].y);
+          }
+      }
+      for (; t <= j; ++t) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          double2 b = ld_d2_stream(basis + (size_t)t * plane + o + 2 * L * v);
+          double2 hh = ld_d2(h + t * ldv + 2 * q + 2 * L * v);
+          s[v].x = fma(b.x, hh.x, s[v].x);
+          s[v].y = fma(b.y, hh.y, s[v].y);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        double2* wp = reinterpret_cast<double2*>(w + o + 2 * L * v);
+        double2 x = *wp;
+        x.x -= s[v].x;
+        x.y -= s[v].y;
+        *wp = x;
+        if (NORM) {
+          acc[v].x += x.x * x.x;
+          acc[v].y += x.y * x.y;
+        }
+      }
+    }
+  }
+  if (NORM) {
+    __shared__ double smem[kRowWarps * SDB_MAX_BATCH];
+    block_partial<L, VPL>(acc, smem, partials, 0, nblocks, ldv);
+  }
+}
+
+// reorth = "none": w' = w - alpha v_j into wdst, ||w'||^2 partials.
+template <int L, int VPL>
+__global__ void __launch_bounds__(kRowThreads) lz_sub_alpha_norm(const double* __restrict__ vj,
+                                                                 const double* __restrict__ wsrc,
+                                                                 double* __restrict__ wdst, LzState st, int64_t n,
+                                                                 int64_t ldv, int64_t nblocks, double* partials) {
+  constexpr int RPW = 32 / L, RPB = RPW * kRowWarps;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / L, q = lane % L;
+  const int64_t rs = n * blockIdx.x / nblocks, re = n * (blockIdx.x + 1) / nblocks;
+  double2 acc[VPL], al[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    acc[v] = make_double2(0.0, 0.0);
+    al[v] = ld_d2(st.alpha_cur + 2 * q + 2 * L * v);
+  }
+  for (int64_t base = rs; base < re; base += RPB) {
+    const int64_t row = base + warp * RPW + g;
+    if (row < re) {
+      const int64_t o = row * ldv + 2 * q;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        double2 w = ld_d2(wsrc + o + 2 * L * v), p = ld_d2(vj + o + 2 * L * v);
+        w.x -= al[v].x * p.x;
+        w.y -= al[v].y * p.y;
+        st_d2(wdst + o + 2 * L * v, w);
+        acc[v].x += w.x * w.x;
+        acc[v].y += w.y * w.y;
+      }
+    }
+  }
+  __shared__ double smem[kRowWarps * SDB_MAX_BATCH];
+  block_partial<L, VPL>(acc, smem, partials, 0, nblocks, ldv);
+}
+
+// beta_j = ||w||, finiteness, breakdown and truncation logic (lanczos.py:111-128).
+__global__ void lz_beta_reduce(const double* __restrict__ partials, int64_t nblocks, int64_t ldv, int64_t n_vec,
+                               int64_t j, int64_t steps, LzState st, double* __restrict__ beta,
+                               int32_t* __restrict__ steps_done, int32_t* __restrict__ status) {
+  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (l >= ldv) return;
+  const double b = sqrt(sum_blocks(partials, 0, nblocks, ldv, l));
+  if (l >= n_vec || status[l] != SDB_LZ_OK) {
+    st.inv_beta[l] = 0.0;
+    st.beta_prev[l] = 0.0;
+    return;
+  }
+  const double a = st.alpha_cur[l];
+  if (!(isfinite(a) && isfinite(b))) {
+    status[l] = SDB_LZ_NONFINITE;
+    steps_done[l] = (int32_t)(j + 1);
+    st.inv_beta[l] = 0.0;
+    st.beta_prev[l] = 0.0;
+    return;
+  }
+  const double ts = fmax(st.tscale[l], fmax(fabs(a), b));
+  st.tscale[l] = ts;
+  if (j == steps - 1) {
+    beta[l * steps + j] = b;  // beta_next
+    steps_done[l] = (int32_t)steps;
+    st.inv_beta[l] = 0.0;
+    st.beta_prev[l] = b;
+  } else if (b <= 1e-13 * fmax(ts, 1.0)) {
+    beta[l * steps + j] = 0.0;  // truncated: beta_next = 0
+    steps_done[l] = (int32_t)(j + 1);
+    status[l] = SDB_LZ_BREAKDOWN;
+    st.inv_beta[l] = 0.0;
+    st.beta_prev[l] = 0.0;
+  } else {
+    beta[l * steps + j] = b;
+    st.inv_beta[l] = 1.0 / b;
+    st.beta_prev[l] = b;
+  }
+}
+
+// ---- host driver ------------------------------------------------------------------------
+static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+
+struct LzLayout {
+  size_t block, part, h, state, total;
+};
+
+static LzLayout lz_layout(const sdb_matrix* m, int64_t ldv, int64_t steps) {
+  LzLayout L;
+  L.block = align256(sizeof(double) * (size_t)m->n * ldv);
+  L.part = align256(sizeof(double) * (size_t)(steps + 1) * row_blocks(m) * ldv);
+  L.h = align256(sizeof(double) * (size_t)steps * ldv);
+  L.state = align256(sizeof(double) * 4 * (size_t)ldv);
+  L.total = 2 * L.block + L.part + L.h + L.state;
+  return L;
+}
+
+template <class View>
+static int lz_launch_spmm(const View& A, const Geometry& g, const double* wprev, const double* vprev, double* vj,
+                          double* wout, const LzState& st, int first, double c, double inv_d, int64_t n,
+                          int64_t nblocks, double* part, cudaStream_t s) {
+#define SDB_LZ_CASE(LL, VV)                                                                                    \
+  lz_spmm<View, LL, VV><<<(unsigned)nblocks, kRowThreads, 0, s>>>(A, wprev, vprev, vj, wout, st, first, c, inv_d, \
+                                                                 n, g.ldv, nblocks, part)
+  SDB_GEOMETRY_DISPATCH(g, SDB_LZ_CASE);
+#undef SDB_LZ_CASE
+  return SDB_OK;
+}
+
+static int lz_launch_proj(int nv, bool sub_alpha, bool norm, const double* basis, const double* wsrc, double* wdst,
+                          const LzState& st, int64_t j, int64_t n, int64_t ldv, int64_t nrb, double* part,
+                          int64_t norm_slot, cudaStream_t s) {
+  dim3 grid((unsigned)((j + 1 + kProjWarps - 1) / kProjWarps), (unsigned)nrb);
+  dim3 block(kProjWarps * 32);
+#define SDB_PROJ(NVV, SA, NO)                                                                             \
+  if (nv == NVV && sub_alpha == SA && norm == NO) {                                                       \
+    lz_proj<NVV, SA, NO><<<grid, block, 0, s>>>(basis, wsrc, wdst, st, j, n, ldv, nrb, part, norm_slot); \
+    return SDB_OK;                                                                                        \
+  }
+#define SDB_PROJ_NV(NVV) SDB_PROJ(NVV, true, false) SDB_PROJ(NVV, false, false) SDB_PROJ(NVV, true, true)
+  SDB_PROJ_NV(1) SDB_PROJ_NV(2) SDB_PROJ_NV(3) SDB_PROJ_NV(4)
+#undef SDB_PROJ_NV
+#undef SDB_PROJ
+  return fail(SDB_EUNSUPPORTED, "no projection kernel for ldv=%lld", (long long)ldv);
+}
+
+static int lz_launch_update(const Geometry& g, bool norm, const double* basis, double* w, const double* h, int64_t j,
+                            int64_t n, int64_t nblocks, double* part, cudaStream_t s) {
+  if (norm) {
+#define SDB_UP_CASE(LL, VV) \
+  lz_update<LL, VV, true><<<(unsigned)nblocks, kRowThreads, 0, s>>>(basis, w, h, j, n, g.ldv, nblocks, part)
+    SDB_GEOMETRY_DISPATCH(g, SDB_UP_CASE);
+#undef SDB_UP_CASE
+  } else {
+#define SDB_UP_CASE(LL, VV) \
+  lz_update<LL, VV, false><<<(unsigned)nblocks, kRowThreads, 0, s>>>(basis, w, h, j, n, g.ldv, nblocks, part)
+    SDB_GEOMETRY_DISPATCH(g, SDB_UP_CASE);
+#undef SDB_UP_CASE
+  }
+  return SDB_OK;
+}
+
+}  // namespace sdb
+
+using namespace sdb;
+
+extern "C" {
+
+int sdb_lanczos_workspace_size(const sdb_matrix* m, int64_t n_vec, int64_t steps, size_t* bytes) {
+  SDB_REQUIRE(m && bytes, "NULL argument");
+  SDB_REQUIRE(n_vec >= 1 && n_vec <= SDB_MAX_BATCH, "n_vec must lie in [1, %d] per batch", SDB_MAX_BATCH);
+  SDB_REQUIRE(steps >= 1, "need at least one Lanczos step");
+  *bytes = lz_layout(m, choose_geometry(n_vec).ldv, steps).total;
+  return SDB_OK;
+}
+
+int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t steps, int reorth, const double* v0, double* basis,
+                double* alpha, double* beta, int32_t* steps_done, int32_t* status, void* workspace,
+                size_t workspace_bytes, void* stream) {
+  SDB_REQUIRE(m && v0 && basis && alpha && beta && steps_done && status, "NULL argument");
+  SDB_REQUIRE(reorth == SDB_REORTH_FULL || reorth == SDB_REORTH_SELECTIVE || reorth == SDB_REORTH_NONE,
+              "unknown reorth mode %d", reorth);
+  SDB_REQUIRE(steps >= 1, "need at least one Lanczos step");
+  SDB_REQUIRE(d != 0.0, "spectral halfwidth must be non-zero");
+  SDB_REQUIRE(steps <= m->n, "steps=%lld exceeds matrix dimension %lld", (long long)steps, (long long)m->n);
+  size_t need = 0;
+  int rc = sdb_lanczos_workspace_size(m, n_vec, steps, &need);
+  if (rc) return rc;
+  SDB_REQUIRE(workspace && workspace_bytes >= need, "workspace too small (%zu < %zu bytes)", workspace_bytes, need);
+  DeviceGuard dg(m->device);
+  if (!dg.ok) return fail(SDB_ECUDA, "cannot select CUDA device %d", m->device);
+  cudaStream_t s = (cudaStream_t)stream;
+
+  const Geometry g = choose_geometry(n_vec);
+  const int64_t ldv = g.ldv, n = m->n, nrb = row_blocks(m);
+  const int nv = (int)((ldv + 63) / 64);
+  const LzLayout lay = lz_layout(m, ldv, steps);
+  char* p = (char*)workspace;
+  double* W0 = (double*)p;
+  double* W1 = (double*)(p + lay.block);
+  double* part = (double*)(p + 2 * lay.block);
+  double* h = (double*)(p + 2 * lay.block + lay.part);
+  double* stp = (double*)(p + 2 * lay.block + lay.part + lay.h);
+  LzState st{stp, stp + ldv, stp + 2 * ldv, stp + 3 * ldv};
+  const size_t plane = (size_t)n * ldv;
+  const int64_t norm_slot = steps;
+
+  SDB_CUDA(cudaMemsetAsync(alpha, 0, sizeof(double) * n_vec * steps, s));
+  SDB_CUDA(cudaMemsetAsync(beta, 0, sizeof(double) * n_vec * steps, s));
+#define SDB_SN_CASE(LL, VV) lz_start_norm<LL, VV><<<(unsigned)nrb, kRowThreads, 0, s>>>(v0, n, ldv, nrb, part)
+  SDB_GEOMETRY_DISPATCH(g, SDB_SN_CASE);
+#undef SDB_SN_CASE
+  SDB_CHECK_LAUNCH();
+  const int rblk = (int)((ldv + 127) / 128);
+  lz_start_reduce<<<rblk, 128, 0, s>>>(part, nrb, ldv, n_vec, st, steps_done, status);
+  SDB_CHECK_LAUNCH();
+
+  StencilView sv{};
+  CsrView cv{};
+  if (m->format == SDB_FMT_CSR) cv = make_csr_view(m); else sv = make_stencil_view(m);
+
+  const double* wraw = v0;
+  for (int64_t j = 0; j < steps; ++j) {
+    double* vj = basis + (size_t)j * plane;
+    const double* vprev = j > 0 ? basis + (size_t)(j - 1) * plane : nullptr;
+    if (m->format == SDB_FMT_CSR)
+      rc = lz_launch_spmm(cv, g, wraw, vprev, vj, W1, st, j == 0, c, 1.0 / d, n, nrb, part, s);
+    else
+      rc = lz_launch_spmm(sv, g, wraw, vprev, vj, W1, st, j == 0, c, 1.0 / d, n, nrb, part, s);
+    if (rc) return rc;
+    SDB_CHECK_LAUNCH();
+    lz_alpha_reduce<<<rblk, 128, 0, s>>>(part, nrb, ldv, n_vec, j, steps, st, alpha, status);
+    SDB_CHECK_LAUNCH();
+    const int hblk = (int)(((j + 1) * ldv + 255) / 256);
+    if (reorth == SDB_REORTH_FULL) {
+      // pass 1: w' = w - alpha v_j -> W0, h = V^T w'; w' -= V h
+      if ((rc = lz_launch_proj(nv, true, false, basis, W1, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
+      SDB_CHECK_LAUNCH();
+      lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
+      SDB_CHECK_LAUNCH();
+      if ((rc = lz_launch_update(g, false, basis, W0, h, j, n, nrb, part, s))) return rc;
+      SDB_CHECK_LAUNCH();
+      // pass 2: h = V^T w; w -= V h; ||w||^2
+      if ((rc = lz_launch_proj(nv, false, false, basis, W0, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
+      SDB_CHECK_LAUNCH();
+      lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
+      SDB_CHECK_LAUNCH();
+      if ((rc = lz_launch_update(g, true, basis, W0, h, j, n, nrb, part, s))) return rc;
+      SDB_CHECK_LAUNCH();
+    } else if (reorth == SDB_REORTH_SELECTIVE) {
+      if ((rc = lz_launch_proj(nv, true, true, basis, W1, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
+      SDB_CHECK_LAUNCH();
+      lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 1, norm_slot);
+      SDB_CHECK_LAUNCH();
+      if ((rc = lz_launch_update(g, true, basis, W0, h, j, n, nrb, part, s))) return rc;
+      SDB_CHECK_LAUNCH();
+    } else {
+#define SDB_NONE_CASE(LL, VV) \
+  lz_sub_alpha_norm<LL, VV><<<(unsigned)nrb, kRowThreads, 0, s>>>(vj, W1, W0, st, n, ldv, nrb, part)
+      SDB_GEOMETRY_DISPATCH(g, SDB_NONE_CASE);
+#undef SDB_NONE_CASE
+      SDB_CHECK_LAUNCH();
+    }
+    lz_beta_reduce<<<rblk, 128, 0, s>>>(part, nrb, ldv, n_vec, j, steps, st, beta, steps_done, status);
+    SDB_CHECK_LAUNCH();
+    wraw = W0;
+  }
+  return SDB_OK;
+}
+
+}  // extern "C"

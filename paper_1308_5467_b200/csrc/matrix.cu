@@ -1,0 +1,311 @@
+// matrix.cu — library plumbing and the sparse-matrix layer.
+//
+// Reference: SparseSymmetricMatrix (matrix.py:35-109) stores a SciPy CSR with
+// both triangles; its matvec is `csr @ x` (matrix.py:101-102), i.e. SciPy
+// csr_matvec: y_i = sum over the row's entries in storage order.  We keep the
+// CSR exactly as given (row order and in-row order) so the per-row sums run in
+// the same order, narrowed to int32 indices on the device.
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+
+namespace sdb {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  cudaGetLastError();  // clear sticky-free errors
+  const char* base = strrchr(file, '/');
+  return fail(e == cudaErrorMemoryAllocation ? SDB_ENOMEM : SDB_ECUDA, "CUDA error %s (%s) in %s at %s:%d",
+              cudaGetErrorName(e), cudaGetErrorString(e), what, base ? base + 1 : file, line);
+}
+
+int num_sms(int device) {
+  static std::mutex mu;
+  static std::vector<int> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  if (device < 0) device = 0;
+  if ((int)cache.size() <= device) cache.resize(device + 1, 0);
+  if (cache[device] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess || v <= 0) v = 148;
+    cache[device] = v;
+  }
+  return cache[device];
+}
+
+int64_t row_blocks(const sdb_matrix* m) {
+  // 4 resident row-range blocks per SM; never fewer rows than one block
+  // iteration per block for small matrices.
+  int64_t b = 4LL * num_sms(m->device);
+  int64_t by_rows = (m->n + 63) / 64;
+  if (by_rows < b) b = by_rows;
+  return b < 1 ? 1 : b;
+}
+
+Geometry choose_geometry(int64_t n_vec) {
+  // Wide blocks: one warp per row, VPL double2 per lane.
+  if (n_vec > 64) {
+    int vpl = (int)((n_vec + 63) / 64);
+    return Geometry{32, vpl, 64LL * vpl};
+  }
+  // Narrow blocks: pick the padded width 2*L*VPL (VPL <= 4) with the least
+  // padding, preferring more lanes per row (fewer rows per warp).
+  Geometry best{1, 1, 1LL << 40};
+  for (int L = 32; L >= 1; L >>= 1) {
+    for (int vpl = 1; vpl <= 4; ++vpl) {
+      int64_t ldv = 2LL * L * vpl;
+      if (ldv < n_vec) continue;
+      if (ldv < best.ldv) best = Geometry{L, vpl, ldv};
+      break;
+    }
+  }
+  return best;
+}
+
+}  // namespace sdb
+
+using namespace sdb;
+
+namespace {
+
+__global__ void narrow_i64_kernel(const int64_t* __restrict__ src, int32_t* __restrict__ dst, int64_t count,
+                                  int64_t limit, int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t v = src[i];
+    if (v < 0 || v >= limit) atomicExch(bad, 1);
+    dst[i] = (int32_t)v;
+  }
+}
+
+__global__ void check_i32_kernel(const int32_t* __restrict__ src, int64_t count, int64_t limit, int* bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t v = src[i];
+    if (v < 0 || v >= limit) atomicExch(bad, 1);
+  }
+}
+
+__global__ void pack_kernel(const double* __restrict__ pt, int64_t n_vec, int64_t n, int64_t ldv,
+                            double* __restrict__ block) {
+  // pt: n_vec x n ; block: n x ldv.  32x32 tiles through shared memory.
+  __shared__ double tile[32][33];
+  int64_t r0 = (int64_t)blockIdx.x * 32;  // row of block (= index into n)
+  int64_t c0 = (int64_t)blockIdx.y * 32;  // column of block (= probe)
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    int64_t l = c0 + j, i = r0 + threadIdx.x;
+    tile[j][threadIdx.x] = (l < n_vec && i < n) ? pt[l * n + i] : 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    int64_t i = r0 + j, l = c0 + threadIdx.x;
+    if (i < n && l < ldv) block[i * ldv + l] = tile[threadIdx.x][j];
+  }
+}
+
+__global__ void unpack_kernel(const double* __restrict__ block, int64_t n, int64_t ldv, int64_t n_vec,
+                              double* __restrict__ pt) {
+  __shared__ double tile[32][33];
+  int64_t r0 = (int64_t)blockIdx.x * 32;
+  int64_t c0 = (int64_t)blockIdx.y * 32;
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    int64_t i = r0 + j, l = c0 + threadIdx.x;
+    tile[j][threadIdx.x] = (i < n && l < n_vec) ? block[i * ldv + l] : 0.0;
+  }
+  __syncthreads();
+  for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+    int64_t l = c0 + j, i = r0 + threadIdx.x;
+    if (l < n_vec && i < n) pt[l * n + i] = tile[threadIdx.x][j];
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sdb_last_error(void) { return g_last_error.c_str(); }
+
+int sdb_version(void) { return 1; }
+
+int64_t sdb_block_ldv(int64_t n_vec) {
+  if (n_vec < 1 || n_vec > SDB_MAX_BATCH) return -1;
+  return choose_geometry(n_vec).ldv;
+}
+
+int sdb_matrix_create_csr(int device, int64_t n, int64_t nnz, const int64_t* indptr, const void* indices,
+                          int index_bits, const double* values, void* stream, sdb_matrix** out) {
+  SDB_REQUIRE(out != nullptr, "out must not be NULL");
+  *out = nullptr;
+  SDB_REQUIRE(n >= 1, "matrix dimension must be positive (got %lld)", (long long)n);
+  SDB_REQUIRE(nnz >= 0, "nnz must be non-negative");
+  SDB_REQUIRE(nnz < (1LL << 31) && n < (1LL << 31), "matrix too large for int32 CSR (n=%lld, nnz=%lld)",
+              (long long)n, (long long)nnz);
+  SDB_REQUIRE(index_bits == 32 || index_bits == 64, "index_bits must be 32 or 64");
+  SDB_REQUIRE(indptr != nullptr, "indptr must not be NULL");
+  SDB_REQUIRE(nnz == 0 || (indices != nullptr && values != nullptr), "indices/values must not be NULL");
+  // host-side structural checks on the row pointer (n+1 entries, cheap)
+  SDB_REQUIRE(indptr[0] == 0 && indptr[n] == nnz, "indptr must start at 0 and end at nnz");
+  std::vector<int32_t> rp((size_t)n + 1);
+  for (int64_t i = 0; i <= n; ++i) {
+    if (i > 0 && indptr[i] < indptr[i - 1]) return fail(SDB_EINVAL, "indptr must be non-decreasing");
+    rp[(size_t)i] = (int32_t)indptr[i];
+  }
+  DeviceGuard g(device);
+  if (!g.ok) return fail(SDB_ECUDA, "cannot select CUDA device %d", device);
+  cudaStream_t s = (cudaStream_t)stream;
+
+  sdb_matrix* m = new sdb_matrix();
+  m->device = device;
+  m->format = SDB_FMT_CSR;
+  m->n = n;
+  m->nnz = nnz;
+  auto cleanup = [&](int code) {
+    sdb_matrix_destroy(m);
+    return code;
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&m->rowptr, sizeof(int32_t) * (n + 1))) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMalloc(rowptr)", __FILE__, __LINE__));
+  size_t nz = (size_t)(nnz > 0 ? nnz : 1);
+  if ((e = cudaMalloc(&m->colidx, sizeof(int32_t) * nz)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMalloc(colidx)", __FILE__, __LINE__));
+  if ((e = cudaMalloc(&m->values, sizeof(double) * nz)) != cudaSuccess)
+    return cleanup(cuda_fail(e, "cudaMalloc(values)", __FILE__, __LINE__));
+  if ((e = cudaMemcpyAsync(m->rowptr, rp.data(), sizeof(int32_t) * (n + 1), cudaMemcpyHostToDevice, s)) !=
+      cudaSuccess)
+    return cleanup(cuda_fail(e, "upload rowptr", __FILE__, __LINE__));
+  if (nnz > 0) {
+    if ((e = cudaMemcpyAsync(m->values, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return cleanup(cuda_fail(e, "upload values", __FILE__, __LINE__));
+    int* bad = nullptr;
+    if ((e = cudaMalloc(&bad, sizeof(int))) != cudaSuccess) return cleanup(cuda_fail(e, "cudaMalloc", __FILE__, __LINE__));
+    cudaMemsetAsync(bad, 0, sizeof(int), s);
+    if (index_bits == 32) {
+      e = cudaMemcpyAsync(m->colidx, indices, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) {
+        check_i32_kernel<<<1024, 256, 0, s>>>(m->colidx, nnz, n, bad);
+        e = cudaGetLastError();
+      }
+    } else {
+      // stage int64 indices in chunks and narrow on the device
+      const int64_t chunk = 1LL << 26;
+      int64_t* tmp = nullptr;
+      int64_t cn = nnz < chunk ? nnz : chunk;
+      e = cudaMalloc(&tmp, sizeof(int64_t) * cn);
+      for (int64_t off = 0; e == cudaSuccess && off < nnz; off += chunk) {
+        int64_t cnt = (nnz - off) < chunk ? (nnz - off) : chunk;
+        e = cudaMemcpyAsync(tmp, (const int64_t*)indices + off, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) {
+          narrow_i64_kernel<<<1024, 256, 0, s>>>(tmp, m->colidx + off, cnt, n, bad);
+          e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);  // tmp is reused
+      }
+      if (tmp) cudaFree(tmp);
+    }
+    int hbad = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    cudaFree(bad);
+    if (e != cudaSuccess) return cleanup(cuda_fail(e, "upload indices", __FILE__, __LINE__));
+    if (hbad) return cleanup(fail(SDB_EINVAL, "column index out of range [0, %lld)", (long long)n));
+  } else {
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cleanup(cuda_fail(e, "sync", __FILE__, __LINE__));
+  }
+  *out = m;
+  return SDB_OK;
+}
+
+int sdb_matrix_create_stencil(int device, const sdb_stencil_desc* desc, const double* diag, void* stream,
+                              sdb_matrix** out) {
+  SDB_REQUIRE(out != nullptr && desc != nullptr && diag != nullptr, "NULL argument");
+  *out = nullptr;
+  SDB_REQUIRE(desc->nx >= 1 && desc->ny >= 1 && desc->nz >= 1, "stencil grid dims must be positive");
+  SDB_REQUIRE(desc->n_offsets >= 0 && desc->n_offsets <= 26, "stencil supports at most 26 off-centre points");
+  int64_t n = desc->nx * desc->ny * desc->nz;
+  SDB_REQUIRE(n < (1LL << 31), "stencil grid too large");
+  for (int o = 0; o < desc->n_offsets; ++o)
+    for (int a = 0; a < 3; ++a)
+      SDB_REQUIRE(desc->offsets[o][a] >= -1 && desc->offsets[o][a] <= 1, "stencil offsets must lie in [-1,1]");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(SDB_ECUDA, "cannot select CUDA device %d", device);
+  cudaStream_t s = (cudaStream_t)stream;
+  sdb_matrix* m = new sdb_matrix();
+  m->device = device;
+  m->format = SDB_FMT_STENCIL;
+  m->n = n;
+  m->nnz = n * (desc->n_offsets + 1);
+  m->st.nx = desc->nx;
+  m->st.ny = desc->ny;
+  m->st.nz = desc->nz;
+  m->st.n_off = desc->n_offsets;
+  memcpy(m->st.off, desc->offsets, sizeof(m->st.off));
+  memcpy(m->st.w, desc->weights, sizeof(m->st.w));
+  cudaError_t e = cudaMalloc(&m->diag, sizeof(double) * n);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(m->diag, diag, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) {
+    int code = cuda_fail(e, "upload stencil diagonal", __FILE__, __LINE__);
+    sdb_matrix_destroy(m);
+    return code;
+  }
+  *out = m;
+  return SDB_OK;
+}
+
+int sdb_matrix_get_info(const sdb_matrix* m, sdb_matrix_info* info) {
+  SDB_REQUIRE(m != nullptr && info != nullptr, "NULL argument");
+  info->n = m->n;
+  info->nnz = m->nnz;
+  info->format = m->format;
+  info->device = m->device;
+  if (m->format == SDB_FMT_CSR)
+    info->bytes = 12 * m->nnz + 4 * (m->n + 1);
+  else
+    info->bytes = 8 * m->n;
+  return SDB_OK;
+}
+
+void sdb_matrix_destroy(sdb_matrix* m) {
+  if (!m) return;
+  DeviceGuard g(m->device);
+  if (m->rowptr) cudaFree(m->rowptr);
+  if (m->colidx) cudaFree(m->colidx);
+  if (m->values) cudaFree(m->values);
+  if (m->diag) cudaFree(m->diag);
+  delete m;
+}
+
+int sdb_pack_probes(const double* probes_t, int64_t n_vec, int64_t n, int64_t ldv, double* block, void* stream) {
+  SDB_REQUIRE(probes_t && block, "NULL argument");
+  SDB_REQUIRE(n_vec >= 1 && n >= 1 && ldv >= n_vec, "bad pack shape");
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((ldv + 31) / 32));
+  pack_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(probes_t, n_vec, n, ldv, block);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+int sdb_unpack_block(const double* block, int64_t n, int64_t ldv, int64_t n_vec, double* out_t, void* stream) {
+  SDB_REQUIRE(out_t && block, "NULL argument");
+  SDB_REQUIRE(n_vec >= 1 && n >= 1 && ldv >= n_vec, "bad unpack shape");
+  dim3 grid((unsigned)((n + 31) / 32), (unsigned)((n_vec + 31) / 32));
+  unpack_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(block, n, ldv, n_vec, out_t);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,200 @@
+// rowgroup.cuh — the row-group thread mapping shared by the block kernels.
+//
+// A probe block is n x ldv fp64, row-major.  A "row group" is L lanes of one
+// warp (L a power of two <= 32) that together hold one row: lane q owns the
+// double2 columns 2*(q + v*L), v < VPL, so every load of a row is one
+// coalesced run of 16*L bytes per v.  32/L rows share a warp.
+#pragma once
+#include "common.cuh"
+
+namespace sdb {
+
+constexpr int kRowThreads = 256;
+constexpr int kRowWarps = kRowThreads / 32;
+
+// Sum per-thread column accumulators over every row the block touched and
+// write one partial row (ldv doubles) at partials[(slot*nblocks + block)*ldv].
+// Lanes sharing q hold the same columns: xor-shuffle them together, then add
+// the warps in warp order through shared memory (fixed order, deterministic).
+// Must be called by every thread of the block.
+template <int L, int VPL>
+__device__ __forceinline__ void block_partial(double2 (&acc)[VPL], double* smem, double* partials, int64_t slot,
+                                              int64_t nblocks, int64_t ldv) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, q = lane % L;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+#pragma unroll
+    for (int off = L; off < 32; off <<= 1) {
+      acc[v].x += __shfl_xor_sync(0xffffffffu, acc[v].x, off);
+      acc[v].y += __shfl_xor_sync(0xffffffffu, acc[v].y, off);
+    }
+  }
+  if (lane < L) {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      int col = 2 * (q + v * L);
+      smem[warp * ldv + col] = acc[v].x;
+      smem[warp * ldv + col + 1] = acc[v].y;
+    }
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < ldv; col += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kRowWarps; ++w) s += smem[w * ldv + col];
+    partials[(slot * nblocks + blockIdx.x) * ldv + col] = s;
+  }
+  __syncthreads();
+}
+
+// Sum one partial slot over blocks in block order.
+__device__ __forceinline__ double sum_blocks(const double* __restrict__ partials, int64_t slot, int64_t nblocks,
+                                             int64_t ldv, int64_t l) {
+  const double* p = partials + slot * nblocks * ldv + l;
+  double s = 0.0;
+  for (int64_t b = 0; b < nblocks; ++b) s += p[b * ldv];
+  return s;
+}
+
+// ---- matrix views: y[row] = sum_k a_{row,k} x[k] for the lane's columns ------
+// CSR: the row's entries are summed in storage order (SciPy csr_matvec order,
+// matrix.py:101-102).  The L lanes of a row group load up to L (col, value)
+// pairs cooperatively and broadcast them with shuffles; U gathers per lane
+// are issued before they are consumed.  Every lane of the warp must call
+// this (rows past the end pass valid = false).
+struct CsrView {
+  const int32_t* __restrict__ rowptr;
+  const int32_t* __restrict__ colidx;
+  const double* __restrict__ vals;
+};
+
+template <int L, int VPL>
+__device__ __forceinline__ void spmv_row(const CsrView& A, int64_t row, bool valid, int safe,
+                                         const double* __restrict__ x, int64_t ldv, int q, double2 (&y)[VPL]) {
+  constexpr int U = L < 4 ? L : (VPL >= 3 ? 2 : 4);
+  const int beg = valid ? A.rowptr[row] : 0;
+  const int cnt = valid ? A.rowptr[row + 1] - beg : 0;
+  const int maxcnt = __reduce_max_sync(0xffffffffu, cnt);
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) y[v] = make_double2(0.0, 0.0);
+  for (int k0 = 0; k0 < maxcnt; k0 += L) {
+    const int kk = k0 + q;
+    int col = safe;
+    double av = 0.0;
+    if (kk < cnt) {
+      col = __ldg(A.colidx + beg + kk);
+      av = __ldg(A.vals + beg + kk);
+    }
+    const int nloc = min(L, maxcnt - k0);
+    for (int t0 = 0; t0 < nloc; t0 += U) {
+      int ct[U];
+      double at[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ct[u] = __shfl_sync(0xffffffffu, col, t0 + u, L);
+        at[u] = __shfl_sync(0xffffffffu, av, t0 + u, L);
+      }
+      double2 xv[U][VPL];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const double* xr = x + (int64_t)ct[u] * ldv + 2 * q;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) xv[u][v] = ld_d2(xr + 2 * L * v);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          y[v].x = fma(at[u], xv[u][v].x, y[v].x);
+          y[v].y = fma(at[u], xv[u][v].y, y[v].y);
+        }
+      }
+    }
+  }
+}
+
+// Periodic constant-coefficient stencil, (A x)_p = diag[p] x_p + sum_o w_o x_{p+o}
+// on an nx*ny*nz torus (nx fastest).  Terms are summed in the order of the
+// column index each offset produces for an interior point, the diagonal at
+// its sorted place -- the storage order the CSR form of the same operator
+// would have away from the periodic wrap.
+struct StencilView {
+  int64_t nx, ny, nz;
+  int n_off;
+  int center_pos;  // offsets whose column precedes the diagonal
+  int32_t dx[26], dy[26], dz[26];
+  double w[26];
+  const double* diag;
+};
+
+template <int L, int VPL>
+__device__ __forceinline__ void spmv_row(const StencilView& S, int64_t row, bool valid, int safe,
+                                         const double* __restrict__ x, int64_t ldv, int q, double2 (&y)[VPL]) {
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) y[v] = make_double2(0.0, 0.0);
+  if (!valid) return;
+  const int64_t ix = row % S.nx;
+  const int64_t iy = (row / S.nx) % S.ny;
+  const int64_t iz = row / (S.nx * S.ny);
+  const double dg = __ldg(S.diag + row);
+  for (int o = 0; o <= S.n_off; ++o) {
+    double wt;
+    int64_t col;
+    if (o == S.center_pos) {
+      wt = dg;
+      col = row;
+    } else {
+      const int oo = o < S.center_pos ? o : o - 1;
+      int64_t jx = ix + S.dx[oo], jy = iy + S.dy[oo], jz = iz + S.dz[oo];
+      jx = jx < 0 ? jx + S.nx : (jx >= S.nx ? jx - S.nx : jx);
+      jy = jy < 0 ? jy + S.ny : (jy >= S.ny ? jy - S.ny : jy);
+      jz = jz < 0 ? jz + S.nz : (jz >= S.nz ? jz - S.nz : jz);
+      col = (jz * S.ny + jy) * S.nx + jx;
+      wt = S.w[oo];
+    }
+    const double* xr = x + col * ldv + 2 * q;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      double2 xv = ld_d2(xr + 2 * L * v);
+      y[v].x = fma(wt, xv.x, y[v].x);
+      y[v].y = fma(wt, xv.y, y[v].y);
+    }
+  }
+}
+
+StencilView make_stencil_view(const sdb_matrix* m);
+inline CsrView make_csr_view(const sdb_matrix* m) { return CsrView{m->rowptr, m->colidx, m->values}; }
+
+// Instantiate F<L, VPL> for the runtime geometry.
+#define SDB_GEOMETRY_DISPATCH(g, CASE)                                                                  \
+  do {                                                                                                  \
+    switch ((g).L * 8 + (g).VPL) {                                                                      \
+      case 32 * 8 + 1: CASE(32, 1); break;                                                              \
+      case 32 * 8 + 2: CASE(32, 2); break;                                                              \
+      case 32 * 8 + 3: CASE(32, 3); break;                                                              \
+      case 32 * 8 + 4: CASE(32, 4); break;                                                              \
+      case 16 * 8 + 1: CASE(16, 1); break;                                                              \
+      case 16 * 8 + 2: CASE(16, 2); break;                                                              \
+      case 16 * 8 + 3: CASE(16, 3); break;                                                              \
+      case 16 * 8 + 4: CASE(16, 4); break;                                                              \
+      case 8 * 8 + 1: CASE(8, 1); break;                                                                \
+      case 8 * 8 + 2: CASE(8, 2); break;                                                                \
+      case 8 * 8 + 3: CASE(8, 3); break;                                                                \
+      case 8 * 8 + 4: CASE(8, 4); break;                                                                \
+      case 4 * 8 + 1: CASE(4, 1); break;                                                                \
+      case 4 * 8 + 2: CASE(4, 2); break;                                                                \
+      case 4 * 8 + 3: CASE(4, 3); break;                                                                \
+      case 4 * 8 + 4: CASE(4, 4); break;                                                                \
+      case 2 * 8 + 1: CASE(2, 1); break;                                                                \
+      case 2 * 8 + 2: CASE(2, 2); break;                                                                \
+      case 2 * 8 + 3: CASE(2, 3); break;                                                                \
+      case 2 * 8 + 4: CASE(2, 4); break;                                                                \
+      case 1 * 8 + 1: CASE(1, 1); break;                                                                \
+      case 1 * 8 + 2: CASE(1, 2); break;                                                                \
+      case 1 * 8 + 3: CASE(1, 3); break;                                                                \
+      case 1 * 8 + 4: CASE(1, 4); break;                                                                \
+      default: return fail(SDB_EUNSUPPORTED, "no kernel for row geometry L=%d VPL=%d", (g).L, (g).VPL); \
+    }                                                                                                   \
+  } while (0)
+
+}  // namespace sdb

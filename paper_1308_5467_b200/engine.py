@@ -1,0 +1,215 @@
+"""Device plumbing between the reference-shaped API and the C ABI.
+
+PyTorch is used only for device memory, pinned host buffers and streams; all
+arithmetic on the hot path runs in the kernels of ``libspecdens_b200.so``.
+"""
+
+import ctypes
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .errors import NumericalFailure
+from .operators import device_matrix, resolve
+from .stochastic import draw_block
+
+SPECTRUM_ESCAPE_HINT = (
+    "the recurrence produced non-finite moments, which usually means the "
+    "spectrum escapes the mapped interval [-1, 1]; widen the spectral "
+    "interval (larger safety margin or more Lanczos steps for the bounds)"
+)
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def require_cuda(device=None):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_1308_5467_b200 needs a CUDA device (sm_100a); no GPU is visible and there is no CPU fallback"
+        )
+    _native.load()
+    if device is None:
+        device = torch.cuda.current_device()
+    return int(device)
+
+
+def stream_ptr(device):
+    torch = _torch()
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def block_ldv(n_vec):
+    v = _native.load().sdb_block_ldv(int(n_vec))
+    if v < 0:
+        raise ValueError(f"probe batch size {n_vec} outside [1, {_native.SDB_MAX_BATCH}]")
+    return int(v)
+
+
+def batches(n_vec, batch=_native.SDB_MAX_BATCH):
+    """Contiguous probe ranges of at most ``batch`` probes."""
+    return [(s, min(batch, n_vec - s)) for s in range(0, n_vec, batch)]
+
+
+@dataclass
+class Staged:
+    """A probe batch resident on the device as an n x ldv block."""
+
+    block: object   # torch float64 (n, ldv)
+    ldv: int
+    h2d_bytes: int
+
+
+def stage_probes(source, start, count, n, device, stream):
+    """Draw probes start..start+count-1 on the host and pack them on device."""
+    torch = _torch()
+    if int(source.dim) != n:
+        raise ValueError(f"probe dimension {source.dim} does not match operator dimension {n}")
+    host = draw_block(source, start, count)
+    if not isinstance(host, torch.Tensor):
+        host = torch.from_numpy(np.ascontiguousarray(host, dtype=np.float64))
+    dev_t = torch.empty((count, n), dtype=torch.float64, device=device)
+    dev_t.copy_(host, non_blocking=True)
+    ldv = block_ldv(count)
+    block = torch.empty((n, ldv), dtype=torch.float64, device=device)
+    _native.call("sdb_pack_probes", ptr(dev_t), count, n, ldv, ptr(block), stream)
+    # keep the host buffer alive until the stream has consumed it
+    block._sdb_keepalive = (host, dev_t)
+    return Staged(block=block, ldv=ldv, h2d_bytes=8 * count * n)
+
+
+def pack_device_probes(probes_t, device, stream):
+    """Pack an on-device (count, n) probe tensor into an n x ldv block."""
+    torch = _torch()
+    count, n = probes_t.shape
+    ldv = block_ldv(count)
+    block = torch.empty((n, ldv), dtype=torch.float64, device=device)
+    _native.call("sdb_pack_probes", ptr(probes_t), count, n, ldv, ptr(block), stream)
+    return Staged(block=block, ldv=ldv, h2d_bytes=0)
+
+
+class Workspace:
+    """Grow-only device scratch buffer (one per device)."""
+
+    _per_device = {}
+
+    @classmethod
+    def get(cls, device, nbytes):
+        torch = _torch()
+        buf = cls._per_device.get(device)
+        if buf is None or buf.numel() < nbytes:
+            cls._per_device.pop(device, None)
+            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+            cls._per_device[device] = buf
+        return buf
+
+    @classmethod
+    def release(cls):
+        cls._per_device.clear()
+
+
+# ---------------------------------------------------------------------------
+# KPM moments
+
+
+@dataclass
+class MomentRun:
+    zeta_pp: object        # torch (n_vec, degree+1) on device
+    n: int
+    resolved: object
+    matvecs_per_probe: int
+    step_ms: float         # CUDA-event time of the recurrence kernels
+    h2d_bytes: int
+    dm: object
+
+
+def run_chebyshev(op, degree, source, n_vec, mode, device=None, probes=None, time_steps=False):
+    """Per-probe Chebyshev moments of the resolved operator on one device.
+
+    ``probes`` optionally supplies an on-device (n_vec, n) tensor instead of
+    drawing from ``source`` (used by the benchmark's device-resident leg and
+    the multi-GPU shard, which pass their own slice).
+    """
+    torch = _torch()
+    device = require_cuda(device)
+    res = resolve(op)
+    n = res.dim
+    if res.d == 0.0:
+        raise ValueError("spectral halfwidth must be non-zero")
+    with torch.cuda.device(device):
+        stream = stream_ptr(device)
+        dm = device_matrix(res.base, device, stream)
+        zeta_pp = torch.empty((n_vec, degree + 1), dtype=torch.float64, device=device)
+        lib = _native.load()
+        step_ms_total = 0.0
+        h2d = 0
+        for start, count in batches(n_vec):
+            if probes is not None:
+                staged = pack_device_probes(probes[start:start + count], device, stream)
+            else:
+                staged = stage_probes(source, start, count, n, device, stream)
+            h2d += staged.h2d_bytes
+            need = ctypes.c_size_t()
+            _native.check(lib.sdb_cheb_workspace_size(dm.handle, count, degree, mode, ctypes.byref(need)))
+            ws = Workspace.get(device, need.value)
+            out = zeta_pp[start:start + count]
+            ms = ctypes.c_float(0.0)
+            _native.check(lib.sdb_cheb_moments(dm.handle, res.c, res.d, count, degree, mode, ptr(staged.block),
+                                               ptr(out), ptr(ws), ws.numel(), stream,
+                                               ctypes.byref(ms) if time_steps else None))
+            step_ms_total += ms.value
+        per_probe = (degree + 1) // 2 if mode == _native.SDB_CHEB_DOUBLING else degree
+    return MomentRun(zeta_pp=zeta_pp, n=n, resolved=res, matvecs_per_probe=per_probe, step_ms=step_ms_total,
+                     h2d_bytes=h2d, dm=dm)
+
+
+def credit_counters(resolved, n_vec, per_probe):
+    for c in resolved.counters:
+        c.count += n_vec * per_probe
+
+
+def mean_moments(zeta_pp, device):
+    """Probe-ordered mean (kpm.py:135) on device; returns (zeta_dev, flag_dev)."""
+    torch = _torch()
+    n_vec, m1 = zeta_pp.shape
+    zeta = torch.empty(m1, dtype=torch.float64, device=device)
+    flag = torch.zeros(1, dtype=torch.int32, device=device)
+    _native.call("sdb_moments_mean", ptr(zeta_pp), n_vec, m1 - 1, ptr(zeta), ptr(flag), stream_ptr(device))
+    return zeta, flag
+
+
+def kpm_density_device(zeta_dev, degree, n, damping, t_dev, d, device):
+    """mu = coefficients(zeta), values = Clenshaw(mu, t)/sqrt(1-t^2), density = values/d."""
+    torch = _torch()
+    stream = stream_ptr(device)
+    mu = torch.empty(degree + 1, dtype=torch.float64, device=device)
+    _native.call("sdb_kpm_coefficients", ptr(zeta_dev), degree, n, damping, ptr(mu), stream)
+    n_pts = t_dev.numel()
+    values = torch.empty(n_pts, dtype=torch.float64, device=device)
+    density = torch.empty(n_pts, dtype=torch.float64, device=device)
+    _native.call("sdb_chebyshev_series", ptr(mu), degree, ptr(t_dev), n_pts, 1, float(d), ptr(values),
+                 ptr(density), stream)
+    return mu, values, density
+
+
+def to_device(arr, device):
+    torch = _torch()
+    return torch.as_tensor(np.ascontiguousarray(arr, dtype=np.float64)).to(device, non_blocking=False)
+
+
+class Timer:
+    def __init__(self):
+        self.t0 = time.perf_counter()
+
+    def elapsed(self):
+        return time.perf_counter() - self.t0

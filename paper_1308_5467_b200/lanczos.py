@@ -1,0 +1,307 @@
+"""Lanczos quadrature on the GPU: drop-in for specdens/lanczos.py (hot path).
+
+  lanczos_factorize      lanczos.py:67-131   -> sdb_lanczos (batch of one)
+  prefix_factorization   lanczos.py:134-149  (pure slicing, kept on the host)
+  ritz_quadrature        lanczos.py:152-159  -> sdb_ritz_quadrature (first-row QL)
+  pool_ritz_quadratures  lanczos.py:170-177  -> sdb_pool_nodes
+  blur_nodes             lanczos.py:180-187  -> sdb_blur_nodes
+  lanczos_dos            lanczos.py:198-219  -> all probes in lock-step batches,
+                                                 quadrature, pooling and blur on device
+
+Haydock / CDOS (lanczos.py:222-368) are outside the hot path.
+"""
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from . import engine as E
+from .density import DEFAULT_GRID_POINTS, RegularizationKernel, SpectralDensityEstimate, interval_grid
+from .errors import NumericalFailure
+from .operators import device_matrix, resolve
+
+BREAKDOWN_RTOL = 1e-13
+REORTH_MODES = ("full", "selective", "none")
+
+# cap on the device memory one batch's Lanczos basis may take
+BASIS_BUDGET_BYTES = 64 << 30
+
+
+@dataclass
+class TridiagonalFactorization:
+    """alpha (M), beta (M-1), beta_next, optional basis (n x M), breakdown (lanczos.py:33-51)."""
+
+    alpha: np.ndarray
+    beta: np.ndarray
+    beta_next: float
+    basis: np.ndarray = None
+    breakdown: bool = False
+
+    @property
+    def steps(self):
+        return len(self.alpha)
+
+
+@dataclass
+class RitzQuadrature:
+    theta: np.ndarray
+    tau_sq: np.ndarray
+    probe_index: int = None
+
+
+@dataclass
+class LanczosBatch:
+    """Device outputs of one lock-step batch."""
+
+    alpha: object        # (count, steps)
+    beta: object         # (count, steps)
+    steps_done: object   # int32 (count,)
+    status: object       # int32 (count,)
+    basis: object        # (steps, n, ldv) or None once released
+    ldv: int
+
+
+def _check_args(reorth, steps, dim):
+    if reorth not in REORTH_MODES:
+        raise ValueError(f"unknown reorth mode {reorth!r}, expected one of {REORTH_MODES}")
+    if steps < 1:
+        raise ValueError("need at least one Lanczos step")
+    if steps > dim:
+        raise ValueError(f"steps={steps} exceeds matrix dimension {dim}")
+
+
+def _run_batch(dm, res, staged, count, steps, reorth, device, stream):
+    torch = E._torch()
+    lib = _native.load()
+    n = res.dim
+    basis = torch.empty((steps, n, staged.ldv), dtype=torch.float64, device=device)
+    alpha = torch.empty((count, steps), dtype=torch.float64, device=device)
+    beta = torch.empty((count, steps), dtype=torch.float64, device=device)
+    steps_done = torch.empty(count, dtype=torch.int32, device=device)
+    status = torch.empty(count, dtype=torch.int32, device=device)
+    need = ctypes.c_size_t()
+    _native.check(lib.sdb_lanczos_workspace_size(dm.handle, count, steps, ctypes.byref(need)))
+    ws = E.Workspace.get(device, need.value)
+    _native.check(lib.sdb_lanczos(dm.handle, res.c, res.d, count, steps, _native.SDB_REORTH[reorth],
+                                  E.ptr(staged.block), E.ptr(basis), E.ptr(alpha), E.ptr(beta), E.ptr(steps_done),
+                                  E.ptr(status), E.ptr(ws), ws.numel(), stream))
+    return LanczosBatch(alpha=alpha, beta=beta, steps_done=steps_done, status=status, basis=basis, ldv=staged.ldv)
+
+
+def _raise_for_status(status, steps_done, first_index=0):
+    """Reproduce the reference's first error in probe order."""
+    bad = np.nonzero((status == _native.SDB_LZ_ZERO_START) | (status == _native.SDB_LZ_NONFINITE))[0]
+    if bad.size == 0:
+        return
+    l = int(bad[0])
+    if status[l] == _native.SDB_LZ_ZERO_START:
+        raise ValueError("starting vector must be nonzero")
+    raise NumericalFailure(f"non-finite Lanczos recurrence at step {int(steps_done[l])}")
+
+
+def _batch_size(n, steps, n_vec):
+    per_col = 8 * steps * n
+    cap = max(1, BASIS_BUDGET_BYTES // max(per_col, 1))
+    return int(max(1, min(_native.SDB_MAX_BATCH, n_vec, cap)))
+
+
+def lanczos_factorize(op, v0, steps, reorth="full", device=None):
+    """``steps`` Lanczos iterations from v0 (lanczos.py:67-131), on the GPU."""
+    if reorth not in REORTH_MODES:
+        raise ValueError(f"unknown reorth mode {reorth!r}, expected one of {REORTH_MODES}")
+    if steps < 1:
+        raise ValueError("need at least one Lanczos step")
+    if steps > op.dim:
+        raise ValueError(f"steps={steps} exceeds matrix dimension {op.dim}")
+    v0 = np.asarray(v0, dtype=float)
+    if np.linalg.norm(v0) == 0.0:
+        raise ValueError("starting vector must be nonzero")
+    torch = E._torch()
+    device = E.require_cuda(device)
+    res = resolve(op)
+    n = res.dim
+    if v0.shape != (n,):
+        raise ValueError(f"starting vector has shape {v0.shape}, expected ({n},)")
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        dm = device_matrix(res.base, device, stream)
+        probes = E.to_device(v0.reshape(1, n), device)
+        staged = E.pack_device_probes(probes, device, stream)
+        out = _run_batch(dm, res, staged, 1, steps, reorth, device, stream)
+        status = out.status.cpu().numpy()
+        sd = out.steps_done.cpu().numpy()
+        _raise_for_status(status, sd)
+        m = int(sd[0])
+        alpha = out.alpha[0, :m].cpu().numpy()
+        beta_all = out.beta[0].cpu().numpy()
+        basis = out.basis[:m, :, 0].transpose(0, 1).contiguous().cpu().numpy() if m else None
+    for c in res.counters:
+        c.count += m
+    if status[0] == _native.SDB_LZ_BREAKDOWN:
+        return TridiagonalFactorization(alpha=alpha, beta=beta_all[: m - 1].copy(), beta_next=0.0, basis=basis,
+                                        breakdown=True)
+    return TridiagonalFactorization(alpha=alpha, beta=beta_all[: steps - 1].copy(), beta_next=float(beta_all[steps - 1]),
+                                    basis=basis)
+
+
+def prefix_factorization(fact, steps):
+    """The factorization the first ``steps`` iterations would give (lanczos.py:134-149)."""
+    m = min(steps, fact.steps)
+    if m == fact.steps:
+        return fact
+    return TridiagonalFactorization(
+        alpha=fact.alpha[:m].copy(),
+        beta=fact.beta[: m - 1].copy(),
+        beta_next=float(fact.beta[m - 1]),
+        basis=None if fact.basis is None else fact.basis[:, :m],
+    )
+
+
+def _ritz_device(alpha, beta, steps_done, m, device, stream):
+    torch = E._torch()
+    count = steps_done.numel()
+    theta = torch.empty((count, m), dtype=torch.float64, device=device)
+    tau2 = torch.empty((count, m), dtype=torch.float64, device=device)
+    _native.call("sdb_ritz_quadrature", E.ptr(alpha), E.ptr(beta), E.ptr(steps_done), count, m, E.ptr(theta),
+                 E.ptr(tau2), stream)
+    return theta, tau2
+
+
+def ritz_quadrature(fact, probe_index=None, device=None):
+    """Ritz values and squared first eigenvector components (lanczos.py:152-159)."""
+    torch = E._torch()
+    device = E.require_cuda(device)
+    m = int(fact.steps)
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        a = E.to_device(np.asarray(fact.alpha, dtype=float).reshape(1, m), device)
+        b = np.zeros((1, m))
+        b[0, : m - 1] = np.asarray(fact.beta, dtype=float)[: m - 1]
+        bd = E.to_device(b, device)
+        sd = torch.tensor([m], dtype=torch.int32, device=device)
+        theta, tau2 = _ritz_device(a, bd, sd, m, device, stream)
+        return RitzQuadrature(theta=theta[0].cpu().numpy(), tau_sq=tau2[0].cpu().numpy(), probe_index=probe_index)
+
+
+def _pool_device(theta, tau2, steps_done, divisor, device, stream):
+    torch = E._torch()
+    rows, m = theta.shape
+    nodes = torch.empty(rows * m, dtype=torch.float64, device=device)
+    weights = torch.empty(rows * m, dtype=torch.float64, device=device)
+    count = ctypes.c_int64()
+    _native.call("sdb_pool_nodes", E.ptr(theta), E.ptr(tau2), E.ptr(steps_done), rows, m, float(divisor),
+                 E.ptr(nodes), E.ptr(weights), ctypes.byref(count), stream)
+    return nodes[: count.value], weights[: count.value]
+
+
+def pool_ritz_quadratures(quads, device=None):
+    """Union of per-probe nodes, weights averaged over probes (lanczos.py:170-177)."""
+    if not quads:
+        raise ValueError("no quadratures to pool")
+    torch = E._torch()
+    device = E.require_cuda(device)
+    m = max(len(q.theta) for q in quads)
+    m = max(m, 1)
+    th = np.zeros((len(quads), m))
+    tw = np.zeros((len(quads), m))
+    sd = np.zeros(len(quads), dtype=np.int32)
+    for i, q in enumerate(quads):
+        k = len(q.theta)
+        th[i, :k] = q.theta
+        tw[i, :k] = q.tau_sq
+        sd[i] = k
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        nodes, weights = _pool_device(E.to_device(th, device), E.to_device(tw, device),
+                                      torch.as_tensor(sd).to(device), len(quads), device, stream)
+        return RitzQuadrature(theta=nodes.cpu().numpy(), tau_sq=weights.cpu().numpy())
+
+
+_KERNEL_CODE = {"gaussian": 0, "lorentzian": 1}
+
+
+def _blur_device(nodes, weights, grid_dev, kind, width, scale, device, stream):
+    torch = E._torch()
+    out = torch.empty_like(grid_dev)
+    _native.call("sdb_blur_nodes", E.ptr(nodes) if nodes.numel() else None,
+                 E.ptr(weights) if weights.numel() else None, nodes.numel(), float(scale), _KERNEL_CODE[kind],
+                 float(width), E.ptr(grid_dev), grid_dev.numel(), E.ptr(out), stream)
+    return out
+
+
+def blur_nodes(theta, weights, grid, kernel, block=512, device=None):
+    """Sum of weighted kernel bumps (lanczos.py:180-187); ``block`` is ignored."""
+    torch = E._torch()
+    device = E.require_cuda(device)
+    grid = np.asarray(grid, dtype=float)
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        out = _blur_device(E.to_device(np.asarray(theta, float).ravel(), device),
+                           E.to_device(np.asarray(weights, float).ravel(), device),
+                           E.to_device(grid.ravel(), device), kernel.kind, kernel.width, 1.0, device, stream)
+        return out.cpu().numpy().reshape(grid.shape)
+
+
+def lanczos_quadrature_device(op, steps, source, n_vec, reorth="full", device=None, probes=None):
+    """All probes' (theta, tau2, steps_done) on device, batched in lock-step.
+
+    Returns (res, theta (n_vec, steps), tau2, steps_done, h2d_bytes).
+    Raises like the reference on zero starting vectors / non-finite runs.
+    """
+    torch = E._torch()
+    device = E.require_cuda(device)
+    res = resolve(op)
+    n = res.dim
+    _check_args(reorth, steps, n)
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        dm = device_matrix(res.base, device, stream)
+        theta = torch.empty((n_vec, steps), dtype=torch.float64, device=device)
+        tau2 = torch.empty((n_vec, steps), dtype=torch.float64, device=device)
+        sd_all = torch.empty(n_vec, dtype=torch.int32, device=device)
+        st_all = torch.empty(n_vec, dtype=torch.int32, device=device)
+        h2d = 0
+        for start, count in E.batches(n_vec, _batch_size(n, steps, n_vec)):
+            if probes is not None:
+                staged = E.pack_device_probes(probes[start:start + count], device, stream)
+            else:
+                staged = E.stage_probes(source, start, count, n, device, stream)
+            h2d += staged.h2d_bytes
+            out = _run_batch(dm, res, staged, count, steps, reorth, device, stream)
+            out.basis = None  # free the basis before the next batch
+            th, tw = _ritz_device(out.alpha, out.beta, out.steps_done, steps, device, stream)
+            theta[start:start + count] = th
+            tau2[start:start + count] = tw
+            sd_all[start:start + count] = out.steps_done
+            st_all[start:start + count] = out.status
+        status = st_all.cpu().numpy()
+        sd = sd_all.cpu().numpy()
+    _raise_for_status(status, sd)
+    return res, theta, tau2, sd_all, h2d
+
+
+def lanczos_dos(op, interval, steps, source, n_vec, sigma, grid=None, threads=None, reorth="full", device=None):
+    """Gaussian-blurred average of per-probe Ritz quadratures (lanczos.py:198-219)."""
+    if not sigma > 0:
+        raise ValueError("sigma must be positive")
+    if grid is None:
+        grid = interval_grid(interval, DEFAULT_GRID_POINTS)
+    grid = np.asarray(grid, dtype=float)
+    torch = E._torch()
+    device = E.require_cuda(device)
+    res, theta, tau2, sd, _ = lanczos_quadrature_device(op, steps, source, n_vec, reorth=reorth, device=device)
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        nodes, weights = _pool_device(theta, tau2, sd, n_vec, device, stream)
+        dens = _blur_device(nodes, weights, E.to_device(grid, device), "gaussian", sigma, 1.0, device, stream)
+        density = dens.cpu().numpy()
+        nodes_h = nodes.cpu().numpy()
+        weights_h = weights.cpu().numpy()
+    for c in res.counters:
+        c.count += int(sd.sum().item())
+    return SpectralDensityEstimate.from_parts(
+        grid, density, grid, density, interval, method="lanczos",
+        params={"M": steps, "n_vec": n_vec, "sigma": sigma, "ritz_nodes": nodes_h, "ritz_weights": weights_h},
+    )

@@ -1,0 +1,400 @@
+"""The operator side of the drop-in boundary.
+
+The reference's plugin API is duck-typed: "anything with a ``dim`` attribute
+and a ``matvec(x)`` method" (specdens/matrix.py:3-6).  Its front door wraps the
+matrix as ``MappedOperator(MatvecCounter(SparseSymmetricMatrix))``
+(compare.py:93-96).  The GPU engine never calls ``matvec``: it walks that
+chain, reads the affine map (c, d) from every ``MappedOperator`` and the CSR
+arrays (or the stencil description) from the innermost matrix, uploads them
+once to a device handle, and adds the analytic MATVEC count to every
+``MatvecCounter`` it passed.  Objects that expose only ``matvec`` cannot be
+offloaded and raise ``TypeError`` (there is no CPU fallback).
+
+The classes below mirror the reference's (matrix.py:35-170) so code written
+against ``specdens`` finds the same names; the reference's own instances are
+accepted as well.  Their ``matvec`` methods exist only for interop with code
+that calls the protocol directly; the engine does not use them.
+"""
+
+import ctypes
+import threading
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _native
+
+
+# ---------------------------------------------------------------------------
+# host-side operator types (mirrors of matrix.py:35-170)
+
+
+@dataclass
+class SparseSymmetricMatrix:
+    """Real symmetric CSR matrix, both triangles stored (matrix.py:35-109)."""
+
+    csr: sp.csr_array
+    symmetric_storage: bool = False
+
+    @classmethod
+    def from_coo(cls, n, rows, cols, vals, symmetric_storage=False):
+        rows = np.asarray(rows, dtype=np.int64)
+        cols = np.asarray(cols, dtype=np.int64)
+        vals = np.asarray(vals, dtype=np.float64)
+        if rows.size and (rows.min() < 0 or cols.min() < 0 or rows.max() >= n or cols.max() >= n):
+            raise ValueError("coordinate index out of range")
+        if symmetric_storage:
+            off = rows != cols
+            rows, cols = np.concatenate([rows, cols[off]]), np.concatenate([cols, rows[off]])
+            vals = np.concatenate([vals, vals[off]])
+        a = sp.coo_array((vals, (rows, cols)), shape=(n, n)).tocsr()
+        a.sum_duplicates()
+        mat = cls(csr=a, symmetric_storage=symmetric_storage)
+        if not mat.is_symmetric():
+            raise ValueError("matrix data is not symmetric")
+        return mat
+
+    @classmethod
+    def from_dense(cls, a):
+        a = np.asarray(a, dtype=float)
+        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+            raise ValueError("dense input must be square")
+        if not np.array_equal(a, a.T):
+            raise ValueError("dense input must be exactly symmetric")
+        return cls(csr=sp.csr_array(a))
+
+    @property
+    def n(self):
+        return self.csr.shape[0]
+
+    @property
+    def dim(self):
+        return self.csr.shape[0]
+
+    def matvec(self, x):  # interop only; the engine never calls it
+        return self.csr @ x
+
+    def is_symmetric(self):
+        return (self.csr != self.csr.T).nnz == 0
+
+
+class StencilOperator:
+    """Periodic constant-coefficient stencil on an nx*ny*nz grid (nx fastest).
+
+    (A x)_p = diag[p] x_p + sum_o weights[o] x_{p + offsets[o]} with periodic
+    wrap.  Not a reference type: it is the matrix-free form of the structured
+    configs (Anderson 7-point, 27-point), satisfies the same protocol, and
+    exposes ``csr`` (built lazily) so the CPU oracle and the reference can run
+    on exactly the same operator.
+    """
+
+    def __init__(self, shape, offsets, weights, diag):
+        self.shape = tuple(int(s) for s in shape)
+        if len(self.shape) != 3 or min(self.shape) < 1:
+            raise ValueError("stencil shape must be three positive extents (nx, ny, nz)")
+        self.offsets = [tuple(int(v) for v in o) for o in offsets]
+        self.weights = [float(w) for w in weights]
+        if len(self.offsets) != len(self.weights) or len(self.offsets) > 26:
+            raise ValueError("need one weight per offset, at most 26 off-centre points")
+        for o in self.offsets:
+            if len(o) != 3 or any(abs(v) > 1 for v in o) or o == (0, 0, 0):
+                raise ValueError(f"bad stencil offset {o}")
+        if len(set(self.offsets)) != len(self.offsets):
+            raise ValueError("duplicate stencil offsets")
+        self.diag = np.ascontiguousarray(diag, dtype=np.float64)
+        nx, ny, nz = self.shape
+        if self.diag.shape != (nx * ny * nz,):
+            raise ValueError("diag must have one entry per grid point")
+        # a stencil offset and its wrap-around image must differ, else the
+        # CSR form would merge entries (needs extent >= 3 along moved axes)
+        for axis in range(3):
+            if any(o[axis] != 0 for o in self.offsets) and self.shape[axis] < 3:
+                raise ValueError("periodic stencils need at least 3 points along every coupled axis")
+        self._csr = None
+
+    @property
+    def dim(self):
+        return int(self.diag.shape[0])
+
+    @property
+    def n(self):
+        return self.dim
+
+    @property
+    def nnz(self):
+        return self.dim * (len(self.offsets) + 1)
+
+    @property
+    def csr(self):
+        """The same operator as a sorted-column CSR array (both triangles)."""
+        if self._csr is None:
+            nx, ny, nz = self.shape
+            n = self.dim
+            p = np.arange(n, dtype=np.int64)
+            ix, iy, iz = p % nx, (p // nx) % ny, p // (nx * ny)
+            cols = [p]
+            vals = [self.diag]
+            for (dx, dy, dz), w in zip(self.offsets, self.weights):
+                jx, jy, jz = (ix + dx) % nx, (iy + dy) % ny, (iz + dz) % nz
+                cols.append((jz * ny + jy) * nx + jx)
+                vals.append(np.full(n, w))
+            cols = np.stack(cols, axis=1)
+            vals = np.stack(vals, axis=1)
+            order = np.argsort(cols, axis=1, kind="stable")
+            cols = np.take_along_axis(cols, order, axis=1)
+            vals = np.take_along_axis(vals, order, axis=1)
+            k = cols.shape[1]
+            indptr = np.arange(0, n * k + 1, k, dtype=np.int64)
+            self._csr = sp.csr_array((vals.ravel(), cols.ravel().astype(np.int32), indptr), shape=(n, n))
+        return self._csr
+
+    def matvec(self, x):  # interop only; the engine never calls it
+        return self.csr @ x
+
+
+class MappedOperator:
+    """B = (A - cI)/d of an operator onto the unit interval (matrix.py:112-126)."""
+
+    def __init__(self, op, interval):
+        self.op = op
+        self.interval = interval
+        self.c = interval.center
+        self.d = interval.halfwidth
+
+    @property
+    def dim(self):
+        return self.op.dim
+
+    def matvec(self, x):  # interop only
+        return (self.op.matvec(x) - self.c * x) / self.d
+
+
+class MatvecCounter:
+    """Counts MATVECs (matrix.py:129-142); the engine adds analytic counts."""
+
+    def __init__(self, op):
+        self.op = op
+        self.count = 0
+
+    @property
+    def dim(self):
+        return self.op.dim
+
+    def matvec(self, x):  # interop only
+        self.count += 1
+        return self.op.matvec(x)
+
+
+class _DenseOperator:
+    def __init__(self, a):
+        self.a = np.asarray(a, dtype=float)
+        self.dim = self.a.shape[0]
+
+    def matvec(self, x):  # interop only
+        return self.a @ x
+
+    def toarray(self):
+        return self.a
+
+
+def as_operator(obj):
+    """Adapt a matrix-like object to the operator protocol (matrix.py:157-165)."""
+    if hasattr(obj, "matvec") and hasattr(obj, "dim"):
+        return obj
+    if isinstance(obj, np.ndarray):
+        return _DenseOperator(obj)
+    if sp.issparse(obj):
+        return SparseSymmetricMatrix(csr=sp.csr_array(obj))
+    raise TypeError(f"cannot interpret {type(obj).__name__} as a linear operator")
+
+
+def apply_spectral_map(op, interval):
+    """(A - cI)/d without copying the matrix (matrix.py:168-170)."""
+    return MappedOperator(as_operator(op), interval)
+
+
+# ---------------------------------------------------------------------------
+# operator chain -> device handle
+
+
+@dataclass
+class ResolvedOperator:
+    """What the engine needs from an operator chain."""
+
+    base: object          # innermost matrix-like object
+    c: float              # B = (A - c I) / d
+    d: float
+    counters: list        # MatvecCounter-like objects to credit
+    dim: int
+
+
+def resolve(op):
+    """Walk MappedOperator / MatvecCounter wrappers down to the matrix.
+
+    Nested maps compose: ((A - c1)/d1 - c2)/d2 = (A - (c1 + c2 d1)) / (d1 d2).
+    """
+    c, d = 0.0, 1.0
+    counters = []
+    obj = op
+    seen = 0
+    while True:
+        seen += 1
+        if seen > 64:
+            raise TypeError("operator chain too deep")
+        if _is_mapped(obj):
+            c_i, d_i = float(obj.c), float(obj.d)
+            # running map (X - c)/d with X = (A' - c_i)/d_i underneath
+            c, d = c_i + c * d_i, d * d_i
+            obj = obj.op
+            continue
+        if _is_counter(obj):
+            counters.append(obj)
+            obj = obj.op
+            continue
+        break
+    base = _base_matrix(obj)
+    dim = int(base.dim) if hasattr(base, "dim") else int(base.shape[0])
+    return ResolvedOperator(base=base, c=c, d=d, counters=counters, dim=dim)
+
+
+def _is_mapped(obj):
+    return hasattr(obj, "op") and hasattr(obj, "c") and hasattr(obj, "d") and hasattr(obj, "matvec")
+
+
+def _is_counter(obj):
+    return hasattr(obj, "op") and hasattr(obj, "count") and hasattr(obj, "matvec") and not _is_mapped(obj)
+
+
+def _base_matrix(obj):
+    if isinstance(obj, StencilOperator):
+        return obj
+    if hasattr(obj, "csr") and sp.issparse(getattr(obj, "csr")):
+        return obj
+    if isinstance(obj, np.ndarray):
+        return _DenseOperator(obj)
+    if hasattr(obj, "a") and isinstance(getattr(obj, "a"), np.ndarray) and hasattr(obj, "matvec"):
+        return obj  # reference _DenseOperator
+    if sp.issparse(obj):
+        return SparseSymmetricMatrix(csr=sp.csr_array(obj))
+    raise TypeError(
+        f"cannot offload operator of type {type(obj).__name__} to the GPU: it exposes no CSR "
+        "arrays or stencil description (only matvec); there is no CPU fallback"
+    )
+
+
+def _csr_arrays(base):
+    if hasattr(base, "csr"):
+        csr = base.csr
+    else:
+        csr = sp.csr_array(np.asarray(base.a, dtype=float))
+    if not isinstance(csr, (sp.csr_array, sp.csr_matrix)):
+        csr = sp.csr_array(csr)
+    n = csr.shape[0]
+    if csr.shape[0] != csr.shape[1]:
+        raise ValueError("matrix must be square")
+    return csr, n
+
+
+class DeviceMatrix:
+    """Owns one ``sdb_matrix`` handle on one CUDA device."""
+
+    def __init__(self, handle, device, n, nnz, fmt, stream_bytes):
+        self.handle = handle
+        self.device = device
+        self.n = n
+        self.nnz = nnz
+        self.format = fmt
+        self.bytes_per_pass = stream_bytes  # M_A: matrix bytes one SpMM streams
+        self._finalizer = weakref.finalize(self, _destroy_handle, handle)
+
+    @classmethod
+    def upload(cls, base, device, stream):
+        lib = _native.load()
+        h = ctypes.c_void_p()
+        if isinstance(base, StencilOperator):
+            desc = _native.SdbStencilDesc()
+            desc.nx, desc.ny, desc.nz = base.shape
+            desc.n_offsets = len(base.offsets)
+            for i, (o, w) in enumerate(zip(base.offsets, base.weights)):
+                for a in range(3):
+                    desc.offsets[i][a] = o[a]
+                desc.weights[i] = w
+            diag = np.ascontiguousarray(base.diag, dtype=np.float64)
+            _native.check(lib.sdb_matrix_create_stencil(device, ctypes.byref(desc), diag.ctypes.data,
+                                                        stream, ctypes.byref(h)))
+        else:
+            csr, n = _csr_arrays(base)
+            indptr = np.ascontiguousarray(csr.indptr, dtype=np.int64)
+            idx = csr.indices
+            if idx.dtype == np.int32:
+                bits = 32
+                idx = np.ascontiguousarray(idx)
+            else:
+                bits = 64
+                idx = np.ascontiguousarray(idx, dtype=np.int64)
+            data = np.ascontiguousarray(csr.data, dtype=np.float64)
+            _native.check(lib.sdb_matrix_create_csr(device, n, int(indptr[-1]), indptr.ctypes.data,
+                                                    idx.ctypes.data if idx.size else None, bits,
+                                                    data.ctypes.data if data.size else None, stream,
+                                                    ctypes.byref(h)))
+        info = _native.SdbMatrixInfo()
+        _native.check(lib.sdb_matrix_get_info(h, ctypes.byref(info)))
+        return cls(h, device, info.n, info.nnz, info.format, info.bytes)
+
+
+def _destroy_handle(h):
+    try:
+        _native.load().sdb_matrix_destroy(h)
+    except Exception:  # interpreter shutdown
+        pass
+
+
+# Cache of device handles keyed by the identity of the host matrix object.
+# Operators are immutable by contract ("SparseSymmetricMatrix
+# is immutable after construction"), so a handle stays valid as long as the
+# host object lives; the entry dies with it.
+_cache_lock = threading.Lock()
+_cache = {}
+
+
+def _cache_key(base, device):
+    if isinstance(base, StencilOperator):
+        arr = base.diag
+        return (id(base), device, arr.ctypes.data, arr.shape[0], "stencil")
+    csr = base.csr if hasattr(base, "csr") else None
+    if csr is not None:
+        return (id(base), device, csr.data.ctypes.data, csr.indices.ctypes.data, csr.nnz, "csr")
+    return None
+
+
+def device_matrix(base, device, stream):
+    """Device handle for a resolved base matrix (cached per host object)."""
+    key = _cache_key(base, device)
+    if key is None:
+        return DeviceMatrix.upload(base, device, stream)
+    with _cache_lock:
+        ent = _cache.get(key)
+        if ent is not None:
+            ref, dm = ent
+            if ref() is base:
+                return dm
+    dm = DeviceMatrix.upload(base, device, stream)
+    try:
+        ref = weakref.ref(base, lambda _r, k=key: _drop(k))
+    except TypeError:  # not weak-referenceable: do not cache
+        return dm
+    with _cache_lock:
+        _cache[key] = (ref, dm)
+    return dm
+
+
+def _drop(key):
+    with _cache_lock:
+        _cache.pop(key, None)
+
+
+def clear_device_cache():
+    with _cache_lock:
+        _cache.clear()

@@ -1,0 +1,142 @@
+"""Generate the golden fixtures by running the REFERENCE itself.
+
+Run in the build container (the reference is importable there, not on the GPU
+box):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Every fixture records the reference's outputs on seeded inputs produced by
+this repo's generators (paper_1308_5467_b200/workloads.py), plus a SHA-256
+of the matrix arrays so a drifting generator is caught.  The oracle is pinned
+against these files by tests/test_oracle_golden.py and the CUDA path by the
+GPU parity tests.
+"""
+
+import hashlib
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+
+import scipy  # noqa: E402
+import specdens  # noqa: E402
+from specdens import (  # noqa: E402
+    ProbeVectorSource,
+    SparseSymmetricMatrix,
+    apply_spectral_map,
+    compute_chebyshev_moments,
+    estimate_dos,
+    evaluate_kpm_dos,
+    lanczos_dos,
+    lanczos_factorize,
+    moments_to_coefficients,
+    moments_via_product_formula,
+)
+from specdens.density import SpectralInterval, interval_grid, unit_grid  # noqa: E402
+
+from paper_1308_5467_b200 import workloads as W  # noqa: E402
+
+
+class Shifted:
+    """A probe source whose probe i is the reference source's probe start+i."""
+
+    def __init__(self, src, start):
+        self.src, self.start, self.dim = src, start, src.dim
+
+    def draw(self, i):
+        return self.src.draw(self.start + i)
+
+
+def csr_digest(csr):
+    h = hashlib.sha256()
+    for a in (csr.indptr.astype(np.int64), csr.indices.astype(np.int64), csr.data.astype(np.float64)):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def ref_matrix(op):
+    return SparseSymmetricMatrix(csr=op.csr)
+
+
+def kpm_case(name, op, kind, n_vec, degree, n_pts, per_probe=2):
+    t0 = time.time()
+    mat = ref_matrix(op)
+    lb, ub = W.gershgorin_interval(op).lambda_lb, W.gershgorin_interval(op).lambda_ub
+    iv = SpectralInterval(lb, ub)
+    src = ProbeVectorSource(kind, seed=0, dim=mat.dim)
+    mapped = apply_spectral_map(mat, iv)
+    direct = compute_chebyshev_moments(mapped, degree, src, n_vec)
+    product = moments_via_product_formula(mapped, degree, src, n_vec)
+    grid = unit_grid(n_pts)
+    dos_d = evaluate_kpm_dos(moments_to_coefficients(direct, "jackson"), iv, grid)
+    dos_p = evaluate_kpm_dos(moments_to_coefficients(product, "jackson"), iv, grid)
+    pp = np.array([compute_chebyshev_moments(mapped, degree, Shifted(src, l), 1).zeta for l in range(per_probe)])
+    out = dict(
+        kind=kind, n_vec=n_vec, degree=degree, n_pts=n_pts, lb=lb, ub=ub,
+        zeta_direct=direct.zeta, zeta_product=product.zeta, per_probe_direct=pp,
+        values_direct=dos_d.values, density_direct=dos_d.density, lambda_grid=dos_d.lambda_grid,
+        values_product=dos_p.values, density_product=dos_p.density,
+        matrix_sha256=csr_digest(mat.csr), n=mat.dim, nnz=mat.csr.nnz,
+    )
+    est = estimate_dos(mat, iv, "kpm-jackson", degree, src, n_vec, grid_points=n_pts)
+    out["estimate_density"] = est.density
+    out["estimate_matvec_count"] = est.params["matvec_count"]
+    est_p = estimate_dos(mat, iv, "kpm-jackson", degree, src, n_vec, grid_points=n_pts, product_formula=True)
+    out["estimate_density_product"] = est_p.density
+    out["estimate_matvec_count_product"] = est_p.params["matvec_count"]
+    print(f"{name}: n={mat.dim} nnz={mat.csr.nnz} {time.time() - t0:.1f}s", flush=True)
+    return out
+
+
+def lanczos_case(name, op, kind, n_vec, steps, sigma, n_pts):
+    t0 = time.time()
+    mat = ref_matrix(op)
+    g = W.gershgorin_interval(op)
+    iv = SpectralInterval(g.lambda_lb, g.lambda_ub)
+    src = ProbeVectorSource(kind, seed=0, dim=mat.dim)
+    grid = interval_grid(iv, n_pts)
+    est = lanczos_dos(mat, iv, steps, src, n_vec, sigma, grid)
+    alphas, betas, bnext = [], [], []
+    for l in range(min(n_vec, 2)):
+        f = lanczos_factorize(mat, src.draw(l), steps)
+        alphas.append(f.alpha)
+        betas.append(f.beta)
+        bnext.append(f.beta_next)
+    est2 = estimate_dos(mat, iv, "lanczos", steps, src, n_vec, sigma=sigma, grid_points=n_pts)
+    print(f"{name}: n={mat.dim} {time.time() - t0:.1f}s", flush=True)
+    return dict(
+        kind=kind, n_vec=n_vec, steps=steps, sigma=sigma, n_pts=n_pts, lb=iv.lambda_lb, ub=iv.lambda_ub,
+        grid=grid, density=est.density, ritz_nodes=est.params["ritz_nodes"],
+        ritz_weights=est.params["ritz_weights"], alpha=np.array(alphas), beta=np.array(betas),
+        beta_next=np.array(bnext), estimate_density=est2.density,
+        estimate_matvec_count=est2.params["matvec_count"], matrix_sha256=csr_digest(mat.csr), n=mat.dim,
+    )
+
+
+def main():
+    meta = dict(numpy=np.__version__, scipy=scipy.__version__, specdens=specdens.__version__,
+                python=sys.version.split()[0])
+    cases = {
+        "c1_kpm": lambda: kpm_case("c1_kpm", W.build_matrix("C1"), "gaussian", 20, 100, 1000),
+        "c2_subset": lambda: kpm_case("c2_subset", W.build_matrix("C2"), "rademacher", 2, 500, 2000),
+        "c3_small": lambda: kpm_case("c3_small", W.dft_like(20000), "gaussian", 4, 200, 2000),
+        "c5_small": lambda: kpm_case("c5_small", W.stencil27_3d(24), "rademacher", 2, 200, 2000),
+        "c4_subset": lambda: lanczos_case("c4_subset", W.build_matrix("C4"), "gaussian", 4, 100, 0.01, 2000),
+        "lanczos_small": lambda: lanczos_case("lanczos_small", W.anderson_3d(8), "gaussian", 6, 40, 0.05, 400),
+    }
+    only = sys.argv[1:]
+    for name, fn in cases.items():
+        if only and name not in only:
+            continue
+        data = fn()
+        data.update({f"meta_{k}": v for k, v in meta.items()})
+        np.savez_compressed(os.path.join(HERE, f"{name}.npz"), **data)
+
+
+if __name__ == "__main__":
+    main()
