@@ -1,0 +1,346 @@
+"""Benchmark: stochastic Chebyshev-moment KPM DOS on the GPU (BASELINE.json metric).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config C2] [--impl reference]
+
+One "step" is one full KPM estimate of the config: all probes' moments (the
+fused recurrence), probe mean, Jackson coefficients and the DOS on the grid.
+Default workload: config 2 (3D Anderson 64^3, W = 16.5, fp64 CSR, M = 500,
+64 Rademacher probes, Jackson damping, 2000 DOS points), product-formula
+(doubling) moments: 250 SpMM steps deliver the 501 moments.
+
+Metric: GNNZ-vec/s = nnz * n_vec * M / t (M = moments delivered).  ``value``
+is measured with the matrix and the probes resident in HBM (L2 flushed
+between steps); ``e2e`` goes through the public ``estimate_dos`` with the
+probes in pinned host memory, copied host->device every step, and the moments
+and density read back every step.  Multi-GPU (torchrun): probe sharding,
+weak scaling -- rank r runs probes [r*n_vec, (r+1)*n_vec), the per-probe
+moments are all-gathered once per step (the only collective) and averaged in
+probe order.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--format", default="csr", choices=["csr", "stencil"])
+    ap.add_argument("--direct", action="store_true", help="direct (non-doubling) moments")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-probes", type=int, default=0)
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def load_traffic(config, fmt):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    v = d.get(f"{config}:{fmt}")
+    return None if v is None else float(v)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_workload(config, fmt):
+    from paper_1308_5467_b200 import SparseSymmetricMatrix, workloads as W
+
+    cfg = W.CONFIGS[config]
+    op = W.build_matrix(config)
+    iv = W.gershgorin_interval(op)
+    if fmt == "csr" and not isinstance(op, SparseSymmetricMatrix):
+        op = SparseSymmetricMatrix(csr=op.csr)
+    return cfg, op, iv
+
+
+def nnz_of(op):
+    return int(op.csr.nnz) if hasattr(op, "csr") and not hasattr(op, "offsets") else int(op.nnz)
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle port; the reference itself is Python and
+# does not travel to the GPU box)
+
+
+def cpu_sample(op, iv, cfg, probes, product):
+    from oracle import specdens_oracle as O
+
+    csr = op.csr
+    t0 = time.perf_counter()
+    O.chebyshev_moments(csr, iv.center, iv.halfwidth, cfg.degree, cfg.probe_kind, 0, probes,
+                        mode="product" if product else "direct")
+    return time.perf_counter() - t0
+
+
+def cpu_baseline(op, iv, cfg, product, probes):
+    secs = cpu_sample(op, iv, cfg, probes, product)
+    gnnz = nnz_of(op) * probes * cfg.degree / secs / 1e9
+    return {"value": gnnz, "unit": "GNNZ-vec/s", "cores": 1, "kind": "port",
+            "sample": f"{cfg.name}: {probes} probes x M={cfg.degree} "
+                      f"({'product formula' if product else 'direct'}), NumPy/SciPy oracle "
+                      f"(scipy csr_matvec, single thread), {secs:.2f} s"}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg, op, iv = build_workload(args.config, "csr")
+    product = not args.direct
+    probes = args.cpu_sample_probes or 2
+    times = []
+    for i in range(args.warmup + args.steps):
+        s = cpu_sample(op, iv, cfg, probes, product)
+        if i >= args.warmup:
+            times.append(s)
+    t = statistics.mean(times)
+    value = nnz_of(op) * probes * cfg.degree / t / 1e9
+    line = {
+        "impl": "reference", "metric": "Chebyshev moment steps: nnz*n_vec*deg/s (GNNZ-vec/s)", "value": value,
+        "unit": "GNNZ-vec/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_dict(cfg, "csr", product, op, args.gpus),
+        "cpu_baseline": {"value": value, "unit": "GNNZ-vec/s", "cores": 1, "kind": "port",
+                         "sample": f"each step: {probes} probes x M={cfg.degree} of {cfg.name} on the host, "
+                                   "NumPy/SciPy oracle port of the reference (single thread)"},
+        "e2e": {"value": value, "unit": "GNNZ-vec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def config_dict(cfg, fmt, product, op, n_gpus):
+    return {"workload": f"{cfg.name}: {cfg.description}", "n": int(op.dim), "nnz": nnz_of(op), "degree": cfg.degree,
+            "n_vec_per_gpu": cfg.n_vec, "global_probes": cfg.n_vec * n_gpus, "probe_kind": cfg.probe_kind,
+            "grid_points": cfg.grid_points, "damping": "jackson", "format": fmt,
+            "moments": "product-formula doubling" if product else "direct",
+            "parallelism": f"probe-shard x{n_gpus}", "l2": "flushed between timed steps (256 MB write)",
+            "interval": "Gershgorin"}
+
+
+# ---------------------------------------------------------------------------
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_1308_5467_b200 as sdb
+    from paper_1308_5467_b200 import _native, compare, distributed
+    from paper_1308_5467_b200 import engine as E
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    product = not args.direct
+    cfg, op, iv = build_workload(args.config, args.format)
+    n = op.dim
+    nnz = nnz_of(op)
+    n_vec = cfg.n_vec
+    grid = sdb.unit_grid(cfg.grid_points)
+    src = sdb.ProbeVectorSource(cfg.probe_kind, seed=0, dim=n)
+    first = rank * n_vec
+    # device-resident probes of this rank (drawn once, outside any timing)
+    host = src.draw_block(first, n_vec)
+    probes_dev = host.to(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    mode = _native.SDB_CHEB_DOUBLING if product else _native.SDB_CHEB_DIRECT
+    steps_per_probe = (cfg.degree + 1) // 2 if product else cfg.degree
+    mapped = sdb.apply_spectral_map(op, iv)
+
+    def one_step():
+        run = E.run_chebyshev(mapped, cfg.degree, None, n_vec, mode, device=local, probes=probes_dev,
+                              time_steps=True)
+        zeta_pp = run.zeta_pp
+        if world > 1:
+            zeta_pp = distributed.all_gather_probe_moments(zeta_pp, world)
+        zeta, flag = E.mean_moments(zeta_pp, dev)
+        t_dev = E.to_device(grid, dev) if not hasattr(one_step, "t") else one_step.t
+        one_step.t = t_dev
+        E.kpm_density_device(zeta, cfg.degree, n, _native.SDB_DAMP_JACKSON, t_dev, iv.halfwidth, dev)
+        return run
+
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times, kernel_ms = [], []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            run = one_step()
+            e1.record()
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+            kernel_ms.append(run.step_ms)
+    if world > 1:
+        dist.barrier()
+    t_ms = statistics.mean(times)
+    k_ms = statistics.mean(kernel_ms)
+    if world > 1:
+        tt = torch.tensor([t_ms, k_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms, k_ms = float(tt[0]), float(tt[1])
+    value = world * nnz * n_vec * cfg.degree / (t_ms * 1e-3) / 1e9
+
+    # ---- e2e through the public API (host probes -> device -> host results) ----
+    e2e_src = sdb.ProbeVectorSource(cfg.probe_kind, seed=0, dim=n)
+    if world == 1:
+        def e2e_call():
+            return sdb.estimate_dos(op, iv, "kpm-jackson", cfg.degree, e2e_src, n_vec, grid_points=cfg.grid_points,
+                                    product_formula=product)
+    else:
+        def e2e_call():
+            return distributed.estimate_dos_sharded(op, iv, "kpm-jackson", cfg.degree, e2e_src, n_vec * world,
+                                                    grid_points=cfg.grid_points, product_formula=product)
+    for _ in range(max(1, args.warmup)):
+        e2e_call()
+    torch.cuda.synchronize()
+    e2e_t = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e2e_call()
+        torch.cuda.synchronize()
+        e2e_t.append(time.perf_counter() - t0)
+    e2e_s = statistics.mean(e2e_t)
+    if world > 1:
+        tt = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_s = float(tt[0])
+    e2e_value = world * nnz * n_vec * cfg.degree / e2e_s / 1e9
+    h2d = 8 * n * n_vec + 8 * cfg.grid_points
+    d2h = 8 * (cfg.degree + 1 + 2 * cfg.grid_points + 1)
+
+    # ---- roofline of the dominant kernel (the fused recurrence step) ----
+    dm = run.dm
+    launches = steps_per_probe
+    ldv = E.block_ldv(n_vec)
+    bytes_launch = dm.bytes_per_pass + 24 * n * n_vec + (8 * n * n_vec if not product else 0)
+    avg_launch_s = k_ms * 1e-3 / launches
+    achieved = bytes_launch / avg_launch_s / 1e9
+    peak, peak_kind = load_peaks()
+    traffic = load_traffic(args.config, args.format)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "kernel": "cheb_step_kernel", "peak_source": f"{peak_kind} hbm_gbs",
+            "bytes_per_launch": bytes_launch, "launches_per_step": launches,
+            "avg_launch_us": avg_launch_s * 1e6, "kernel_share_of_step": k_ms / t_ms, "ldv": ldv}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline(op, iv, cfg, product, args.cpu_sample_probes or 4)
+        except Exception as exc:  # the baseline must not sink the GPU line
+            cpu = {"value": None, "unit": "GNNZ-vec/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
+
+    # my kernels per step: pack + steps + reduce + mean + coefficients + series
+    gpu_launches = args.steps * (1 + launches + 1 + 1 + 1 + 1)
+    line = {
+        "metric": "Chebyshev moment steps: nnz*n_vec*deg/s (GNNZ-vec/s)",
+        "value": value, "unit": "GNNZ-vec/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generators, paper_1308_5467_b200/workloads.py)",
+        "config": config_dict(cfg, args.format, product, op, world),
+        "roofline": roof, "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "GNNZ-vec/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": e2e_s * 1e3,
+                "path": "estimate_dos(kpm-jackson) public API; probes from pinned host memory each step; "
+                        "matrix handle resident (uploaded once, cached per host object)"},
+        "gpu_launches": gpu_launches,
+        "clocks": clk.summary(),
+        "step_rate": {"executed_spmm_gnnz_vec_s": world * nnz * n_vec * steps_per_probe / (t_ms * 1e-3) / 1e9},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
