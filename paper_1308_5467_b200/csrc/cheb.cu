@@ -25,6 +25,11 @@ namespace sdb {
 constexpr int kStepThreads = kRowThreads;
 constexpr int kStepWarps = kRowWarps;
 
+// Resident blocks per SM the step kernels are compiled for (register cap).
+__host__ __device__ constexpr int step_min_blocks(int l, int vpl) {
+  return l < 8 ? (vpl == 1 ? 4 : 2) : (vpl == 1 ? 5 : (vpl == 2 ? 4 : 2));
+}
+
 struct StepArgs {
   const double* x;     // w_k                      (gathered)
   const double* prev;  // w_{k-1}                  (row-local; may alias next)
@@ -32,91 +37,312 @@ struct StepArgs {
   const double* v0;    // probes (direct mode dots)
   double c;            // spectral centre
   double inv_d;        // 1/halfwidth
-  int first;           // k == 0: w_1 = B w_0
   int64_t n;
   int64_t ldv;
   int64_t nblocks;
+  int64_t panel;       // rows per panel of the phased schedule
   double* partials;    // [(M+1)][nblocks][ldv]
   int slotA;           // doubling: <w+,w+>, direct: <v0,w+>   (-1: none)
   int slotB;           // doubling: <w+,w>                       (-1: none)
   int slot0;           // step 0: <w0,w0>                        (-1: none)
 };
 
-// Epilogue shared by the CSR and stencil steps: spectral map, recurrence,
-// store, and the fused dot products for one row.
-template <int L, int VPL, int MODE>
-__device__ __forceinline__ void step_epilogue(const StepArgs& a, int64_t row, int q, double2 (&y)[VPL],
-                                              double2 (&accA)[VPL], double2 (&accB)[VPL],
-                                              double2 (&acc0)[VPL]) {
-  const double* xr = a.x + row * a.ldv + 2 * q;
+// Epilogue shared by the CSR and stencil steps, split in two so the row's own
+// operands (x_i for the spectral shift, w_{k-1}, v_0) are requested before
+// the gathers and arrive while they are in flight.  FIRST (k = 0) has no
+// w_{k-1} and additionally accumulates zeta_0 = <v0, v0>.
+template <int VPL>
+struct EpiIn {
+  double2 xi[VPL];
+  double2 wp[VPL];
+  double2 p0[VPL];
+};
+
+template <int L, int VPL, int MODE, bool FIRST>
+__device__ __forceinline__ void epi_load(const StepArgs& a, int64_t row, int q, uint64_t pol, EpiIn<VPL>& e) {
+  const int64_t o = row * a.ldv + 2 * q;
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
-    const int off = 2 * L * v;
-    double2 xi = ld_d2(xr + off);
+    e.xi[v] = ld_d2(a.x + o + 2 * L * v);
+    if (!FIRST) e.wp[v] = ld_d2_once(a.prev + o + 2 * L * v, pol);
+    if (MODE == SDB_CHEB_DIRECT && !FIRST) e.p0[v] = ld_d2_once(a.v0 + o + 2 * L * v, pol);
+  }
+}
+
+template <int L, int VPL, int MODE, bool FIRST>
+__device__ __forceinline__ void epi_finish(const StepArgs& a, int64_t row, int q, const double2 (&y)[VPL],
+                                           const EpiIn<VPL>& e, double2 (&accA)[VPL], double2 (&accB)[VPL],
+                                           double2 (&accZ)[VPL], uint64_t pol) {
+  const int64_t o = row * a.ldv + 2 * q;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+    const double2 xi = e.xi[v];
     // t = (A x - c x)/d  (matrix.py:126); w+ = t (k = 0) or 2 t - w- (kpm.py:105)
-    double tx = (y[v].x - a.c * xi.x) * a.inv_d;
-    double ty = (y[v].y - a.c * xi.y) * a.inv_d;
+    const double tx = (y[v].x - a.c * xi.x) * a.inv_d;
+    const double ty = (y[v].y - a.c * xi.y) * a.inv_d;
     double2 wn;
-    if (a.first) {
-      wn.x = tx;
-      wn.y = ty;
+    if (FIRST) {
+      wn = make_double2(tx, ty);
     } else {
-      double2 wp = *reinterpret_cast<const double2*>(a.prev + row * a.ldv + 2 * q + off);
-      wn.x = 2.0 * tx - wp.x;
-      wn.y = 2.0 * ty - wp.y;
+      wn.x = 2.0 * tx - e.wp[v].x;
+      wn.y = 2.0 * ty - e.wp[v].y;
     }
-    st_d2(a.next + row * a.ldv + 2 * q + off, wn);
+    st_d2_once(a.next + o + 2 * L * v, wn, pol);
     if (MODE == SDB_CHEB_DOUBLING) {
       accA[v].x += wn.x * wn.x;
       accA[v].y += wn.y * wn.y;
-      accB[v].x += wn.x * xi.x;
-      accB[v].y += wn.y * xi.y;
-      acc0[v].x += xi.x * xi.x;
-      acc0[v].y += xi.y * xi.y;
+      if constexpr (MODE == SDB_CHEB_DOUBLING) {
+        accB[v].x += wn.x * xi.x;
+        accB[v].y += wn.y * xi.y;
+      }
     } else {
-      double2 p = ld_d2(a.v0 + row * a.ldv + 2 * q + off);
+      const double2 p = FIRST ? xi : e.p0[v];  // at k = 0 the gathered block is v0
       accA[v].x += p.x * wn.x;
       accA[v].y += p.y * wn.y;
-      acc0[v].x += p.x * p.x;
-      acc0[v].y += p.y * p.y;
+    }
+    if constexpr (FIRST) {
+      accZ[v].x += xi.x * xi.x;
+      accZ[v].y += xi.y * xi.y;
     }
   }
 }
 
-template <int L, int VPL, int MODE>
+template <int L, int VPL, int MODE, bool FIRST>
 __device__ __forceinline__ void step_finish(const StepArgs& a, double2 (&accA)[VPL], double2 (&accB)[VPL],
-                                            double2 (&acc0)[VPL]) {
+                                            double2 (&accZ)[VPL]) {
   __shared__ double smem[kStepWarps * SDB_MAX_BATCH];
   if (a.slotA >= 0) block_partial<L, VPL>(accA, smem, a.partials, a.slotA, a.nblocks, a.ldv);
-  if (MODE == SDB_CHEB_DOUBLING && a.slotB >= 0) block_partial<L, VPL>(accB, smem, a.partials, a.slotB, a.nblocks, a.ldv);
-  if (a.slot0 >= 0) block_partial<L, VPL>(acc0, smem, a.partials, a.slot0, a.nblocks, a.ldv);
+  if constexpr (MODE == SDB_CHEB_DOUBLING) {
+    if (a.slotB >= 0) block_partial<L, VPL>(accB, smem, a.partials, a.slotB, a.nblocks, a.ldv);
+  }
+  if constexpr (FIRST) {
+    if (a.slot0 >= 0) block_partial<L, VPL>(accZ, smem, a.partials, a.slot0, a.nblocks, a.ldv);
+  }
 }
 
-// ---- K1: one recurrence step for the whole probe block ----------------------------
-// Persistent row-range blocks: block b owns rows [n*b/B, n*(b+1)/B) and walks
-// them RPB rows at a time, so the +-1 / +-nx neighbours of a stencil-like
-// pattern are re-read from L1 within the block.
-template <class View, int L, int VPL, int MODE>
-__global__ void __launch_bounds__(kStepThreads, VPL <= 1 ? 4 : (VPL == 2 ? 3 : 2)) cheb_step_kernel(View A, StepArgs a) {
-  constexpr int RPW = 32 / L;            // rows per warp
-  constexpr int RPB = RPW * kStepWarps;  // rows per block iteration
+// Issue U gathers x[col[u]] (this lane's columns), then accumulate them in
+// order: y += w[u] * x[col[u]].
+template <int L, int VPL, int U>
+__device__ __forceinline__ void gather_fma(const double* __restrict__ x, int64_t ldv, int q, const int (&col)[U],
+                                           const double (&w)[U], double2 (&y)[VPL]) {
+  double2 xv[U][VPL];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const double* xr = x + (int64_t)col[u] * ldv + 2 * q;
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) xv[u][v] = ld_d2(xr + 2 * L * v);
+  }
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      y[v].x = fma(w[u], xv[u][v].x, y[v].x);
+      y[v].y = fma(w[u], xv[u][v].y, y[v].y);
+    }
+  }
+}
+
+// ---- K1, CSR form ---------------------------------------------------------------
+// Rows follow the phased-panel schedule (rowgroup.cuh).  The L lanes of a row
+// group load up to L (col, value) pairs of their row cooperatively and
+// broadcast them with shuffles; U gathers are in flight per lane; the row's
+// own operands are requested before the gathers.  Entries are accumulated in
+// storage order (csr_matvec order, matrix.py:101-102).
+template <int L, int VPL, int MODE, bool FIRST>
+__global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_step_csr(CsrView A, StepArgs a) {
+  constexpr int RPW = 32 / L;
+  constexpr int RPB = RPW * kStepWarps;
+  constexpr int U = L < 4 ? L : (VPL == 1 ? 4 : 2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / L, q = lane % L;
-  const int64_t rs = a.n * blockIdx.x / a.nblocks;
-  const int64_t re = a.n * (blockIdx.x + 1) / a.nblocks;
-
-  double2 accA[VPL], accB[VPL], acc0[VPL];
+  const uint64_t pol = policy_evict_first();
+  double2 accA[VPL], accB[VPL], accZ[VPL];
 #pragma unroll
-  for (int v = 0; v < VPL; ++v) accA[v] = accB[v] = acc0[v] = make_double2(0.0, 0.0);
-
-  for (int64_t base = rs; base < re; base += RPB) {
+  for (int v = 0; v < VPL; ++v) accA[v] = accB[v] = accZ[v] = make_double2(0.0, 0.0);
+  for (int64_t ph = 0;; ++ph) {
+    const int64_t p0 = (ph * a.nblocks + blockIdx.x) * a.panel;
+    if (p0 >= a.n) break;
+    const int64_t pend = p0 + a.panel < a.n ? p0 + a.panel : a.n;
+    for (int64_t base = p0; base < pend; base += RPB) {
     const int64_t row = base + warp * RPW + g;
-    const bool valid = row < re;
+    const bool valid = row < pend;
+    const int safe = valid ? (int)row : (int)base;
+    const int beg = valid ? __ldg(A.rowptr + row) : 0;
+    const int cnt = valid ? __ldg(A.rowptr + row + 1) - beg : 0;
+    EpiIn<VPL> e;
+    if (valid) epi_load<L, VPL, MODE, FIRST>(a, row, q, pol, e);
     double2 y[VPL];
-    spmv_row<L, VPL>(A, row, valid, valid ? (int)row : (int)rs, a.x, a.ldv, q, y);
-    if (valid) step_epilogue<L, VPL, MODE>(a, row, q, y, accA, accB, acc0);
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) y[v] = make_double2(0.0, 0.0);
+    const int maxcnt = __reduce_max_sync(0xffffffffu, cnt);
+    for (int k0 = 0; k0 < maxcnt; k0 += L) {
+      const int kk = k0 + q;
+      int colc = safe;
+      double valc = 0.0;
+      if (kk < cnt) {
+        colc = __ldg(A.colidx + beg + kk);
+        valc = __ldg(A.vals + beg + kk);
+      }
+      const int nloc = min(L, maxcnt - k0);
+      for (int t0 = 0; t0 < nloc; t0 += U) {
+        int ct[U];
+        double at[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          ct[u] = __shfl_sync(0xffffffffu, colc, t0 + u, L);
+          at[u] = __shfl_sync(0xffffffffu, valc, t0 + u, L);
+        }
+        gather_fma<L, VPL, U>(a.x, a.ldv, q, ct, at, y);
+      }
+    }
+    if (valid) epi_finish<L, VPL, MODE, FIRST>(a, row, q, y, e, accA, accB, accZ, pol);
+    }
   }
-  step_finish<L, VPL, MODE>(a, accA, accB, acc0);
+  step_finish<L, VPL, MODE, FIRST>(a, accA, accB, accZ);
+}
+
+// ---- K1, periodic stencil form -------------------------------------------------------
+// Terms (off-centre points + diagonal) are ordered by the column index they
+// produce for an interior point; interior rows use the precomputed deltas,
+// rows on a periodic face recompute wrapped coordinates.
+template <int L, int VPL, int MODE, bool FIRST>
+__global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_step_stencil(StencilView S, StepArgs a) {
+  constexpr int RPW = 32 / L;
+  constexpr int RPB = RPW * kStepWarps;
+  constexpr int U = VPL == 1 ? 8 : (VPL == 2 ? 4 : 2);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane / L, q = lane % L;
+  const uint64_t pol = policy_evict_first();
+  const int nx = S.nx, ny = S.ny, nz = S.nz;
+  double2 accA[VPL], accB[VPL], accZ[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) accA[v] = accB[v] = accZ[v] = make_double2(0.0, 0.0);
+  for (int64_t ph = 0;; ++ph) {
+    const int64_t p0 = (ph * a.nblocks + blockIdx.x) * a.panel;
+    if (p0 >= a.n) break;
+    const int64_t pend = p0 + a.panel < a.n ? p0 + a.panel : a.n;
+    for (int64_t base = p0; base < pend; base += RPB) {
+    const int64_t row = base + warp * RPW + g;
+    if (row >= pend) continue;
+    EpiIn<VPL> e;
+    epi_load<L, VPL, MODE, FIRST>(a, row, q, pol, e);
+    const int r32 = (int)row;
+    const int ix = r32 % nx, t = r32 / nx;
+    const int iy = t % ny, iz = t / ny;
+    const bool interior = (!S.mx || (ix > 0 && ix < nx - 1)) && (!S.my || (iy > 0 && iy < ny - 1)) &&
+                          (!S.mz || (iz > 0 && iz < nz - 1));
+    const double dg = __ldg(S.diag + row);
+    double2 y[VPL];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) y[v] = make_double2(0.0, 0.0);
+    for (int o0 = 0; o0 < S.nterms; o0 += U) {
+      int col[U];
+      double w[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int o = o0 + u;
+        col[u] = r32;
+        w[u] = 0.0;
+        if (o < S.nterms) {
+          const int4 tm = __ldg(S.term + o);
+          w[u] = (o == S.center_pos) ? dg : __ldg(S.tw + o);
+          if (interior) {
+            col[u] = r32 + tm.w;
+          } else {
+            int jx = ix + tm.x, jy = iy + tm.y, jz = iz + tm.z;
+            jx = jx < 0 ? jx + nx : (jx >= nx ? jx - nx : jx);
+            jy = jy < 0 ? jy + ny : (jy >= ny ? jy - ny : jy);
+            jz = jz < 0 ? jz + nz : (jz >= nz ? jz - nz : jz);
+            col[u] = (jz * ny + jy) * nx + jx;
+          }
+        }
+      }
+      gather_fma<L, VPL, U>(a.x, a.ldv, q, col, w, y);
+    }
+    epi_finish<L, VPL, MODE, FIRST>(a, row, q, y, e, accA, accB, accZ, pol);
+    }
+  }
+  step_finish<L, VPL, MODE, FIRST>(a, accA, accB, accZ);
+}
+
+// ---- K1, structured-grid forms (7-point faces, 27-point box) -----------------------
+// The term order is fixed at compile time: lexicographic in (dz, dy, dx), which
+// is the sorted-column order of the stencil's CSR form for nx, ny >= 3.  Per
+// row the wrapped neighbour offsets along each axis are computed once; a
+// term's column is then row + xo + yo + zo.
+template <int SHAPE>
+struct GridShape;
+template <>
+struct GridShape<SDB_SHAPE_FACE7> {
+  static constexpr int NT = 7;
+  __host__ __device__ static constexpr int dx(int o) { return o == 2 ? -1 : (o == 4 ? 1 : 0); }
+  __host__ __device__ static constexpr int dy(int o) { return o == 1 ? -1 : (o == 5 ? 1 : 0); }
+  __host__ __device__ static constexpr int dz(int o) { return o == 0 ? -1 : (o == 6 ? 1 : 0); }
+};
+template <>
+struct GridShape<SDB_SHAPE_BOX27> {
+  static constexpr int NT = 27;
+  __host__ __device__ static constexpr int dx(int o) { return o % 3 - 1; }
+  __host__ __device__ static constexpr int dy(int o) { return (o / 3) % 3 - 1; }
+  __host__ __device__ static constexpr int dz(int o) { return o / 9 - 1; }
+};
+
+template <int SHAPE, int L, int VPL, int MODE, bool FIRST>
+__global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_step_grid(StencilView S, StepArgs a) {
+  using G = GridShape<SHAPE>;
+  constexpr int RPW = 32 / L;
+  constexpr int RPB = RPW * kStepWarps;
+  constexpr int U = VPL == 1 ? 4 : 2;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane / L, q = lane % L;
+  const uint64_t pol = policy_evict_first();
+  const int nx = S.nx, ny = S.ny, nz = S.nz, nxy = nx * ny;
+  double2 accA[VPL], accB[VPL], accZ[VPL];
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) accA[v] = accB[v] = accZ[v] = make_double2(0.0, 0.0);
+  for (int64_t ph = 0;; ++ph) {
+    const int64_t p0 = (ph * a.nblocks + blockIdx.x) * a.panel;
+    if (p0 >= a.n) break;
+    const int64_t pend = p0 + a.panel < a.n ? p0 + a.panel : a.n;
+    for (int64_t base = p0; base < pend; base += RPB) {
+      const int64_t row = base + warp * RPW + g;
+      if (row >= pend) continue;
+      EpiIn<VPL> e;
+      epi_load<L, VPL, MODE, FIRST>(a, row, q, pol, e);
+      const int r32 = (int)row;
+      const int ix = r32 % nx, t = r32 / nx;
+      const int iy = t % ny, iz = t / ny;
+      // wrapped offsets for d = -1, +1 along each axis
+      const int xm = ix == 0 ? nx - 1 : -1, xp = ix == nx - 1 ? 1 - nx : 1;
+      const int ym = iy == 0 ? (ny - 1) * nx : -nx, yp = iy == ny - 1 ? (1 - ny) * nx : nx;
+      const int zm = iz == 0 ? (nz - 1) * nxy : -nxy, zp = iz == nz - 1 ? (1 - nz) * nxy : nxy;
+      double2 y[VPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) y[v] = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int o0 = 0; o0 < G::NT; o0 += U) {
+        int col[U];
+        double w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int o = o0 + u;
+          if (o < G::NT) {
+            const int ox = G::dx(o) < 0 ? xm : (G::dx(o) > 0 ? xp : 0);
+            const int oy = G::dy(o) < 0 ? ym : (G::dy(o) > 0 ? yp : 0);
+            const int oz = G::dz(o) < 0 ? zm : (G::dz(o) > 0 ? zp : 0);
+            col[u] = r32 + ox + oy + oz;
+            w[u] = (G::dx(o) == 0 && G::dy(o) == 0 && G::dz(o) == 0) ? __ldg(S.diag + row) : __ldg(S.tw + o);
+          } else {
+            col[u] = r32;
+            w[u] = 0.0;
+          }
+        }
+        gather_fma<L, VPL, U>(a.x, a.ldv, q, col, w, y);
+      }
+      epi_finish<L, VPL, MODE, FIRST>(a, row, q, y, e, accA, accB, accZ, pol);
+    }
+  }
+  step_finish<L, VPL, MODE, FIRST>(a, accA, accB, accZ);
 }
 
 // Degree 0: only zeta_0 = <v0, v0>.
@@ -126,14 +352,13 @@ __global__ void __launch_bounds__(kStepThreads) self_dot_kernel(StepArgs a) {
   constexpr int RPB = RPW * kStepWarps;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / L, q = lane % L;
-  const int64_t rs = a.n * blockIdx.x / a.nblocks;
-  const int64_t re = a.n * (blockIdx.x + 1) / a.nblocks;
   double2 acc[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) acc[v] = make_double2(0.0, 0.0);
-  for (int64_t base = rs; base < re; base += RPB) {
+  const PanelSched sched{a.n, a.nblocks, a.panel};
+  for_each_panel_chunk<RPB>(sched, [&](int64_t base, int64_t pend) {
     const int64_t row = base + warp * RPW + g;
-    if (row < re) {
+    if (row < pend) {
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         double2 p = ld_d2(a.v0 + row * a.ldv + 2 * q + 2 * L * v);
@@ -141,7 +366,7 @@ __global__ void __launch_bounds__(kStepThreads) self_dot_kernel(StepArgs a) {
         acc[v].y += p.y * p.y;
       }
     }
-  }
+  });
   __shared__ double smem[kStepWarps * SDB_MAX_BATCH];
   block_partial<L, VPL>(acc, smem, a.partials, 0, a.nblocks, a.ldv);
 }
@@ -171,21 +396,91 @@ __global__ void moments_mean_kernel(const double* __restrict__ zeta_pp, int64_t 
 }
 
 // ---- host dispatch ------------------------------------------------------------------
-template <int MODE>
+template <int MODE, bool FIRST>
 static int launch_step(const sdb_matrix* m, const Geometry& g, const StencilView* st, const StepArgs& a,
                        cudaStream_t s) {
   dim3 grid((unsigned)a.nblocks), block(kStepThreads);
   if (m->format == SDB_FMT_CSR) {
     const CsrView A = make_csr_view(m);
-#define SDB_STEP_CASE(LL, VV) cheb_step_kernel<CsrView, LL, VV, MODE><<<grid, block, 0, s>>>(A, a)
+#define SDB_STEP_CASE(LL, VV) cheb_step_csr<LL, VV, MODE, FIRST><<<grid, block, 0, s>>>(A, a)
+    SDB_GEOMETRY_DISPATCH(g, SDB_STEP_CASE);
+#undef SDB_STEP_CASE
+  } else if (m->shape == SDB_SHAPE_FACE7) {
+#define SDB_STEP_CASE(LL, VV) cheb_step_grid<SDB_SHAPE_FACE7, LL, VV, MODE, FIRST><<<grid, block, 0, s>>>(*st, a)
+    SDB_GEOMETRY_DISPATCH(g, SDB_STEP_CASE);
+#undef SDB_STEP_CASE
+  } else if (m->shape == SDB_SHAPE_BOX27) {
+#define SDB_STEP_CASE(LL, VV) cheb_step_grid<SDB_SHAPE_BOX27, LL, VV, MODE, FIRST><<<grid, block, 0, s>>>(*st, a)
     SDB_GEOMETRY_DISPATCH(g, SDB_STEP_CASE);
 #undef SDB_STEP_CASE
   } else {
-#define SDB_STEP_CASE(LL, VV) cheb_step_kernel<StencilView, LL, VV, MODE><<<grid, block, 0, s>>>(*st, a)
+#define SDB_STEP_CASE(LL, VV) cheb_step_stencil<LL, VV, MODE, FIRST><<<grid, block, 0, s>>>(*st, a)
     SDB_GEOMETRY_DISPATCH(g, SDB_STEP_CASE);
 #undef SDB_STEP_CASE
   }
   return SDB_OK;
+}
+
+// Blocks for a moment run: every block of the phased schedule must be
+// resident at once (a second wave would break the sliding window), so the
+// count is SMs x (resident blocks per SM of the step kernels), capped by the
+// number of row iterations.  Fixed per (matrix, geometry, GPU model).
+static int64_t step_blocks(const sdb_matrix* m, const Geometry& g, int64_t rpb) {
+  int occ = 0;
+  const void* fns[4] = {};
+  int nf = 0;
+  if (m->format == SDB_FMT_CSR) {
+#define SDB_OCC_CASE(LL, VV)                                                                \
+  fns[0] = (const void*)cheb_step_csr<LL, VV, SDB_CHEB_DOUBLING, true>;                      \
+  fns[1] = (const void*)cheb_step_csr<LL, VV, SDB_CHEB_DOUBLING, false>;                     \
+  fns[2] = (const void*)cheb_step_csr<LL, VV, SDB_CHEB_DIRECT, true>;                        \
+  fns[3] = (const void*)cheb_step_csr<LL, VV, SDB_CHEB_DIRECT, false>;                       \
+  nf = 4
+    [&]() -> int { SDB_GEOMETRY_DISPATCH(g, SDB_OCC_CASE); return 0; }();
+#undef SDB_OCC_CASE
+  } else if (m->shape == SDB_SHAPE_FACE7) {
+#define SDB_OCC_CASE(LL, VV)                                                                 \
+  fns[0] = (const void*)cheb_step_grid<SDB_SHAPE_FACE7, LL, VV, SDB_CHEB_DOUBLING, true>;     \
+  fns[1] = (const void*)cheb_step_grid<SDB_SHAPE_FACE7, LL, VV, SDB_CHEB_DOUBLING, false>;    \
+  fns[2] = (const void*)cheb_step_grid<SDB_SHAPE_FACE7, LL, VV, SDB_CHEB_DIRECT, true>;       \
+  fns[3] = (const void*)cheb_step_grid<SDB_SHAPE_FACE7, LL, VV, SDB_CHEB_DIRECT, false>;      \
+  nf = 4
+    [&]() -> int { SDB_GEOMETRY_DISPATCH(g, SDB_OCC_CASE); return 0; }();
+#undef SDB_OCC_CASE
+  } else if (m->shape == SDB_SHAPE_BOX27) {
+#define SDB_OCC_CASE(LL, VV)                                                                 \
+  fns[0] = (const void*)cheb_step_grid<SDB_SHAPE_BOX27, LL, VV, SDB_CHEB_DOUBLING, true>;     \
+  fns[1] = (const void*)cheb_step_grid<SDB_SHAPE_BOX27, LL, VV, SDB_CHEB_DOUBLING, false>;    \
+  fns[2] = (const void*)cheb_step_grid<SDB_SHAPE_BOX27, LL, VV, SDB_CHEB_DIRECT, true>;       \
+  fns[3] = (const void*)cheb_step_grid<SDB_SHAPE_BOX27, LL, VV, SDB_CHEB_DIRECT, false>;      \
+  nf = 4
+    [&]() -> int { SDB_GEOMETRY_DISPATCH(g, SDB_OCC_CASE); return 0; }();
+#undef SDB_OCC_CASE
+  } else {
+#define SDB_OCC_CASE(LL, VV)                                                                \
+  fns[0] = (const void*)cheb_step_stencil<LL, VV, SDB_CHEB_DOUBLING, true>;                  \
+  fns[1] = (const void*)cheb_step_stencil<LL, VV, SDB_CHEB_DOUBLING, false>;                 \
+  fns[2] = (const void*)cheb_step_stencil<LL, VV, SDB_CHEB_DIRECT, true>;                    \
+  fns[3] = (const void*)cheb_step_stencil<LL, VV, SDB_CHEB_DIRECT, false>;                   \
+  nf = 4
+    [&]() -> int { SDB_GEOMETRY_DISPATCH(g, SDB_OCC_CASE); return 0; }();
+#undef SDB_OCC_CASE
+  }
+  occ = 1 << 20;
+  for (int i = 0; i < nf; ++i) {
+    int o = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, fns[i], kStepThreads, 0) != cudaSuccess || o < 1) o = 1;
+    occ = o < occ ? o : occ;
+  }
+  if (nf == 0) occ = 4;
+  if (const char* env = getenv("SDB_BLOCKS_PER_SM")) {
+    int v = atoi(env);
+    if (v > 0) occ = v;
+  }
+  int64_t b = (int64_t)occ * num_sms(m->device);
+  const int64_t iters = (m->n + rpb - 1) / rpb;
+  if (iters < b) b = iters;
+  return b < 1 ? 1 : b;
 }
 
 static int launch_self_dot(const Geometry& g, const StepArgs& a, cudaStream_t s) {
@@ -195,42 +490,14 @@ static int launch_self_dot(const Geometry& g, const StepArgs& a, cudaStream_t s)
   return SDB_OK;
 }
 
-StencilView make_stencil_view(const sdb_matrix* m) {
-  StencilView s{};
-  s.nx = m->st.nx;
-  s.ny = m->st.ny;
-  s.nz = m->st.nz;
-  s.n_off = m->st.n_off;
-  s.diag = m->diag;
-  // order the off-centre points by the flattened offset dz*nx*ny + dy*nx + dx
-  int idx[26];
-  for (int o = 0; o < s.n_off; ++o) idx[o] = o;
-  auto flat = [&](int o) {
-    return (int64_t)m->st.off[o][2] * s.nx * s.ny + (int64_t)m->st.off[o][1] * s.nx + m->st.off[o][0];
-  };
-  for (int i = 1; i < s.n_off; ++i)
-    for (int j = i; j > 0 && flat(idx[j]) < flat(idx[j - 1]); --j) {
-      int t = idx[j];
-      idx[j] = idx[j - 1];
-      idx[j - 1] = t;
-    }
-  s.center_pos = 0;
-  for (int o = 0; o < s.n_off; ++o) {
-    s.dx[o] = m->st.off[idx[o]][0];
-    s.dy[o] = m->st.off[idx[o]][1];
-    s.dz[o] = m->st.off[idx[o]][2];
-    s.w[o] = m->st.w[idx[o]];
-    if (flat(idx[o]) < 0) s.center_pos = o + 1;
-  }
-  return s;
-}
-
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 static void cheb_layout(const sdb_matrix* m, int64_t ldv, int64_t degree, size_t* block_bytes,
                         size_t* partial_bytes) {
   *block_bytes = align256(sizeof(double) * (size_t)m->n * (size_t)ldv);
-  *partial_bytes = align256(sizeof(double) * (size_t)(degree + 1) * (size_t)row_blocks(m) * (size_t)ldv);
+  // upper bound on step_blocks(): 8 resident 256-thread blocks per SM
+  const int64_t bmax = 8LL * num_sms(m->device);
+  *partial_bytes = align256(sizeof(double) * (size_t)(degree + 1) * (size_t)bmax * (size_t)ldv);
 }
 
 }  // namespace sdb
@@ -277,7 +544,9 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
   a.inv_d = 1.0 / d;
   a.n = m->n;
   a.ldv = g.ldv;
-  a.nblocks = row_blocks(m);
+  const int rpb = (32 / g.L) * kStepWarps;
+  a.nblocks = step_blocks(m, g, rpb);
+  a.panel = panel_rows(m, g.ldv, rpb);
   a.partials = partials;
   StencilView st{};
   if (m->format == SDB_FMT_STENCIL) st = make_stencil_view(m);
@@ -302,16 +571,17 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
     a.x = cur;
     a.prev = prev;
     a.next = next;
-    a.first = (k == 0);
     a.slot0 = (k == 0) ? 0 : -1;
     if (mode == SDB_CHEB_DOUBLING) {
       a.slotB = (2 * k + 1 <= degree) ? (int)(2 * k + 1) : -1;
       a.slotA = (2 * k + 2 <= degree) ? (int)(2 * k + 2) : -1;
-      rc = launch_step<SDB_CHEB_DOUBLING>(m, g, &st, a, s);
+      rc = k == 0 ? launch_step<SDB_CHEB_DOUBLING, true>(m, g, &st, a, s)
+                  : launch_step<SDB_CHEB_DOUBLING, false>(m, g, &st, a, s);
     } else {
       a.slotA = (int)(k + 1);
       a.slotB = -1;
-      rc = launch_step<SDB_CHEB_DIRECT>(m, g, &st, a, s);
+      rc = k == 0 ? launch_step<SDB_CHEB_DIRECT, true>(m, g, &st, a, s)
+                  : launch_step<SDB_CHEB_DIRECT, false>(m, g, &st, a, s);
     }
     if (rc) return rc;
     SDB_CHECK_LAUNCH();

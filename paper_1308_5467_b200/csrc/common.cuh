@@ -10,6 +10,11 @@
 
 namespace sdb {
 
+// stencil shapes with compile-time term order (cheb.cu)
+#define SDB_SHAPE_GENERIC 0
+#define SDB_SHAPE_FACE7 1
+#define SDB_SHAPE_BOX27 2
+
 // ---- error reporting (thread-local message, status codes) ----------------
 void set_error(const std::string& msg);
 int fail(int code, const char* fmt, ...);
@@ -65,9 +70,18 @@ struct sdb_matrix {
   // stencil
   sdb::StencilDev st{};
   double* diag = nullptr;
+  int4* terms = nullptr;      // (dx, dy, dz, interior column delta), sorted by delta
+  double* term_w = nullptr;   // weight per term (diagonal slot unused)
+  int nterms = 0, center_pos = 0, mx = 0, my = 0, mz = 0;
+  int shape = 0;              // SDB_SHAPE_*: specialised grid kernel available
 };
 
 namespace sdb {
+
+// Rows per panel of the phased-panel schedule (rowgroup.cuh) for a block
+// width of ldv doubles and RPB rows per block iteration.  SDB_PANEL_ROWS
+// overrides it (tuning).
+int64_t panel_rows(const sdb_matrix* m, int64_t ldv, int rpb);
 
 // Blocks of the persistent row-range kernels.  Depends on n and the SM count
 // only, so the reduction tree (and hence every bit of the result) is fixed for

@@ -36,16 +36,15 @@ struct LzState {       // per-probe device state, each an ldv-long array
 // ---- start: ||v0|| --------------------------------------------------------------
 template <int L, int VPL>
 __global__ void __launch_bounds__(kRowThreads) lz_start_norm(const double* __restrict__ v0, int64_t n, int64_t ldv,
-                                                             int64_t nblocks, double* partials) {
+                                                             int64_t nblocks, int64_t panel, double* partials) {
   constexpr int RPW = 32 / L, RPB = RPW * kRowWarps;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / L, q = lane % L;
-  const int64_t rs = n * blockIdx.x / nblocks, re = n * (blockIdx.x + 1) / nblocks;
   double2 acc[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) acc[v] = make_double2(0.0, 0.0);
-  for (int64_t base = rs; base < re; base += RPB) {
+  for_each_panel_chunk<RPB>(PanelSched{n, nblocks, panel}, [&](int64_t base, int64_t pend) {
     const int64_t row = base + warp * RPW + g;
-    if (row < re) {
+    if (row < pend) {
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
         double2 p = ld_d2(v0 + row * ldv + 2 * q + 2 * L * v);
@@ -53,7 +52,7 @@ __global__ void __launch_bounds__(kRowThreads) lz_start_norm(const double* __res
         acc[v].y += p.y * p.y;
       }
     }
-  }
+  });
   __shared__ double smem[kRowWarps * SDB_MAX_BATCH];
   block_partial<L, VPL>(acc, smem, partials, 0, nblocks, ldv);
 }
@@ -79,10 +78,9 @@ template <class View, int L, int VPL>
 __global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
     lz_spmm(View A, const double* __restrict__ wprev, const double* __restrict__ vprev, double* __restrict__ vj,
             double* __restrict__ wout, LzState st, int first, double c, double inv_d, int64_t n, int64_t ldv,
-            int64_t nblocks, double* partials) {
+            int64_t nblocks, int64_t panel, double* partials) {
   constexpr int RPW = 32 / L, RPB = RPW * kRowWarps;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / L, q = lane % L;
-  const int64_t rs = n * blockIdx.x / nblocks, re = n * (blockIdx.x + 1) / nblocks;
   double2 ib[VPL], bp[VPL], acc[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
@@ -90,11 +88,11 @@ __global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
     bp[v] = ld_d2(st.beta_prev + 2 * q + 2 * L * v);
     acc[v] = make_double2(0.0, 0.0);
   }
-  for (int64_t base = rs; base < re; base += RPB) {
+  for_each_panel_chunk<RPB>(PanelSched{n, nblocks, panel}, [&](int64_t base, int64_t pend) {
     const int64_t row = base + warp * RPW + g;
-    const bool valid = row < re;
+    const bool valid = row < pend;
     double2 y[VPL];
-    spmv_row<L, VPL>(A, row, valid, valid ? (int)row : (int)rs, wprev, ldv, q, y);
+    spmv_row<L, VPL>(A, row, valid, valid ? (int)row : (int)base, wprev, ldv, q, y);
     if (valid) {
       const int64_t o = row * ldv + 2 * q;
 #pragma unroll
@@ -115,7 +113,7 @@ __global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
         acc[v].y += vv.y * w.y;
       }
     }
-  }
+  });
   __shared__ double smem[kRowWarps * SDB_MAX_BATCH];
   block_partial<L, VPL>(acc, smem, partials, 0, nblocks, ldv);
 }
@@ -225,17 +223,16 @@ __global__ void lz_h_reduce(const double* __restrict__ partials, int64_t nrb, in
 template <int L, int VPL, bool NORM>
 __global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
     lz_update(const double* __restrict__ basis, double* w, const double* __restrict__ h, int64_t j, int64_t n,
-              int64_t ldv, int64_t nblocks, double* partials) {
+              int64_t ldv, int64_t nblocks, int64_t panel, double* partials) {
   constexpr int RPW = 32 / L, RPB = RPW * kRowWarps;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / L, q = lane % L;
-  const int64_t rs = n * blockIdx.x / nblocks, re = n * (blockIdx.x + 1) / nblocks;
   const size_t plane = (size_t)n * ldv;
   double2 acc[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) acc[v] = make_double2(0.0, 0.0);
-  for (int64_t base = rs; base < re; base += RPB) {
+  for_each_panel_chunk<RPB>(PanelSched{n, nblocks, panel}, [&](int64_t base, int64_t pend) {
     const int64_t row = base + warp * RPW + g;
-    if (row < re) {
+    if (row < pend) {
       const int64_t o = row * ldv + 2 * q;
       double2 s[VPL];
 #pragma unroll
@@ -280,7 +277,7 @@ __global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
         }
       }
     }
-  }
+  });
   if (NORM) {
     __shared__ double smem[kRowWarps * SDB_MAX_BATCH];
     block_partial<L, VPL>(acc, smem, partials, 0, nblocks, ldv);
@@ -292,19 +289,19 @@ template <int L, int VPL>
 __global__ void __launch_bounds__(kRowThreads) lz_sub_alpha_norm(const double* __restrict__ vj,
                                                                  const double* __restrict__ wsrc,
                                                                  double* __restrict__ wdst, LzState st, int64_t n,
-                                                                 int64_t ldv, int64_t nblocks, double* partials) {
+                                                                 int64_t ldv, int64_t nblocks, int64_t panel,
+                                                                 double* partials) {
   constexpr int RPW = 32 / L, RPB = RPW * kRowWarps;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / L, q = lane % L;
-  const int64_t rs = n * blockIdx.x / nblocks, re = n * (blockIdx.x + 1) / nblocks;
   double2 acc[VPL], al[VPL];
 #pragma unroll
   for (int v = 0; v < VPL; ++v) {
     acc[v] = make_double2(0.0, 0.0);
     al[v] = ld_d2(st.alpha_cur + 2 * q + 2 * L * v);
   }
-  for (int64_t base = rs; base < re; base += RPB) {
+  for_each_panel_chunk<RPB>(PanelSched{n, nblocks, panel}, [&](int64_t base, int64_t pend) {
     const int64_t row = base + warp * RPW + g;
-    if (row < re) {
+    if (row < pend) {
       const int64_t o = row * ldv + 2 * q;
 #pragma unroll
       for (int v = 0; v < VPL; ++v) {
@@ -316,7 +313,7 @@ __global__ void __launch_bounds__(kRowThreads) lz_sub_alpha_norm(const double* _
         acc[v].y += w.y * w.y;
       }
     }
-  }
+  });
   __shared__ double smem[kRowWarps * SDB_MAX_BATCH];
   block_partial<L, VPL>(acc, smem, partials, 0, nblocks, ldv);
 }
@@ -381,10 +378,10 @@ static LzLayout lz_layout(const sdb_matrix* m, int64_t ldv, int64_t steps) {
 template <class View>
 static int lz_launch_spmm(const View& A, const Geometry& g, const double* wprev, const double* vprev, double* vj,
                           double* wout, const LzState& st, int first, double c, double inv_d, int64_t n,
-                          int64_t nblocks, double* part, cudaStream_t s) {
+                          int64_t nblocks, int64_t panel, double* part, cudaStream_t s) {
 #define SDB_LZ_CASE(LL, VV)                                                                                    \
   lz_spmm<View, LL, VV><<<(unsigned)nblocks, kRowThreads, 0, s>>>(A, wprev, vprev, vj, wout, st, first, c, inv_d, \
-                                                                 n, g.ldv, nblocks, part)
+                                                                 n, g.ldv, nblocks, panel, part)
   SDB_GEOMETRY_DISPATCH(g, SDB_LZ_CASE);
 #undef SDB_LZ_CASE
   return SDB_OK;
@@ -408,15 +405,15 @@ static int lz_launch_proj(int nv, bool sub_alpha, bool norm, const double* basis
 }
 
 static int lz_launch_update(const Geometry& g, bool norm, const double* basis, double* w, const double* h, int64_t j,
-                            int64_t n, int64_t nblocks, double* part, cudaStream_t s) {
+                            int64_t n, int64_t nblocks, int64_t panel, double* part, cudaStream_t s) {
   if (norm) {
 #define SDB_UP_CASE(LL, VV) \
-  lz_update<LL, VV, true><<<(unsigned)nblocks, kRowThreads, 0, s>>>(basis, w, h, j, n, g.ldv, nblocks, part)
+  lz_update<LL, VV, true><<<(unsigned)nblocks, kRowThreads, 0, s>>>(basis, w, h, j, n, g.ldv, nblocks, panel, part)
     SDB_GEOMETRY_DISPATCH(g, SDB_UP_CASE);
 #undef SDB_UP_CASE
   } else {
 #define SDB_UP_CASE(LL, VV) \
-  lz_update<LL, VV, false><<<(unsigned)nblocks, kRowThreads, 0, s>>>(basis, w, h, j, n, g.ldv, nblocks, part)
+  lz_update<LL, VV, false><<<(unsigned)nblocks, kRowThreads, 0, s>>>(basis, w, h, j, n, g.ldv, nblocks, panel, part)
     SDB_GEOMETRY_DISPATCH(g, SDB_UP_CASE);
 #undef SDB_UP_CASE
   }
@@ -457,6 +454,7 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
   const Geometry g = choose_geometry(n_vec);
   const int64_t ldv = g.ldv, n = m->n, nrb = row_blocks(m);
   const int nv = (int)((ldv + 63) / 64);
+  const int64_t panel = panel_rows(m, ldv, (32 / g.L) * kRowWarps);
   const LzLayout lay = lz_layout(m, ldv, steps);
   char* p = (char*)workspace;
   double* W0 = (double*)p;
@@ -470,7 +468,7 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
 
   SDB_CUDA(cudaMemsetAsync(alpha, 0, sizeof(double) * n_vec * steps, s));
   SDB_CUDA(cudaMemsetAsync(beta, 0, sizeof(double) * n_vec * steps, s));
-#define SDB_SN_CASE(LL, VV) lz_start_norm<LL, VV><<<(unsigned)nrb, kRowThreads, 0, s>>>(v0, n, ldv, nrb, part)
+#define SDB_SN_CASE(LL, VV) lz_start_norm<LL, VV><<<(unsigned)nrb, kRowThreads, 0, s>>>(v0, n, ldv, nrb, panel, part)
   SDB_GEOMETRY_DISPATCH(g, SDB_SN_CASE);
 #undef SDB_SN_CASE
   SDB_CHECK_LAUNCH();
@@ -487,9 +485,9 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
     double* vj = basis + (size_t)j * plane;
     const double* vprev = j > 0 ? basis + (size_t)(j - 1) * plane : nullptr;
     if (m->format == SDB_FMT_CSR)
-      rc = lz_launch_spmm(cv, g, wraw, vprev, vj, W1, st, j == 0, c, 1.0 / d, n, nrb, part, s);
+      rc = lz_launch_spmm(cv, g, wraw, vprev, vj, W1, st, j == 0, c, 1.0 / d, n, nrb, panel, part, s);
     else
-      rc = lz_launch_spmm(sv, g, wraw, vprev, vj, W1, st, j == 0, c, 1.0 / d, n, nrb, part, s);
+      rc = lz_launch_spmm(sv, g, wraw, vprev, vj, W1, st, j == 0, c, 1.0 / d, n, nrb, panel, part, s);
     if (rc) return rc;
     SDB_CHECK_LAUNCH();
     lz_alpha_reduce<<<rblk, 128, 0, s>>>(part, nrb, ldv, n_vec, j, steps, st, alpha, status);
@@ -501,25 +499,25 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
       SDB_CHECK_LAUNCH();
       lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
       SDB_CHECK_LAUNCH();
-      if ((rc = lz_launch_update(g, false, basis, W0, h, j, n, nrb, part, s))) return rc;
+      if ((rc = lz_launch_update(g, false, basis, W0, h, j, n, nrb, panel, part, s))) return rc;
       SDB_CHECK_LAUNCH();
       // pass 2: h = V^T w; w -= V h; ||w||^2
       if ((rc = lz_launch_proj(nv, false, false, basis, W0, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
       SDB_CHECK_LAUNCH();
       lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
       SDB_CHECK_LAUNCH();
-      if ((rc = lz_launch_update(g, true, basis, W0, h, j, n, nrb, part, s))) return rc;
+      if ((rc = lz_launch_update(g, true, basis, W0, h, j, n, nrb, panel, part, s))) return rc;
       SDB_CHECK_LAUNCH();
     } else if (reorth == SDB_REORTH_SELECTIVE) {
       if ((rc = lz_launch_proj(nv, true, true, basis, W1, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
       SDB_CHECK_LAUNCH();
       lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 1, norm_slot);
       SDB_CHECK_LAUNCH();
-      if ((rc = lz_launch_update(g, true, basis, W0, h, j, n, nrb, part, s))) return rc;
+      if ((rc = lz_launch_update(g, true, basis, W0, h, j, n, nrb, panel, part, s))) return rc;
       SDB_CHECK_LAUNCH();
     } else {
 #define SDB_NONE_CASE(LL, VV) \
-  lz_sub_alpha_norm<LL, VV><<<(unsigned)nrb, kRowThreads, 0, s>>>(vj, W1, W0, st, n, ldv, nrb, part)
+  lz_sub_alpha_norm<LL, VV><<<(unsigned)nrb, kRowThreads, 0, s>>>(vj, W1, W0, st, n, ldv, nrb, panel, part)
       SDB_GEOMETRY_DISPATCH(g, SDB_NONE_CASE);
 #undef SDB_NONE_CASE
       SDB_CHECK_LAUNCH();

@@ -6,8 +6,10 @@
 // CSR exactly as given (row order and in-row order) so the per-row sums run in
 // the same order, narrowed to int32 indices on the device.
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -58,6 +60,20 @@ int64_t row_blocks(const sdb_matrix* m) {
   return b < 1 ? 1 : b;
 }
 
+int64_t panel_rows(const sdb_matrix* m, int64_t ldv, int rpb) {
+  int64_t p = 0;
+  if (const char* env = getenv("SDB_PANEL_ROWS")) p = atoll(env);
+  const int64_t B = row_blocks(m);
+  (void)B;
+  (void)ldv;
+  // 64-row panels: short enough that the far neighbours of a row are gathered
+  // by other blocks within a few microseconds (L2 hits), long enough for the
+  // +-1 / +-nx neighbours to be L1 hits (measured, tools/mb/spmm_probe.cu)
+  if (p <= 0) p = 64;
+  p = (p + rpb - 1) / rpb * rpb;
+  return p < rpb ? rpb : p;
+}
+
 Geometry choose_geometry(int64_t n_vec) {
   // Wide blocks: one warp per row, VPL double2 per lane.
   if (n_vec > 64) {
@@ -74,6 +90,12 @@ Geometry choose_geometry(int64_t n_vec) {
       if (ldv < best.ldv) best = Geometry{L, vpl, ldv};
       break;
     }
+  }
+  // tuning override: same ldv, different lanes per row
+  if (const char* env = getenv("SDB_LANES")) {
+    int L = atoi(env);
+    if (L >= 1 && L <= 32 && (L & (L - 1)) == 0 && best.ldv % (2 * L) == 0 && best.ldv / (2 * L) <= 4)
+      best = Geometry{L, (int)(best.ldv / (2 * L)), best.ldv};
   }
   return best;
 }
@@ -255,11 +277,63 @@ int sdb_matrix_create_stencil(int device, const sdb_stencil_desc* desc, const do
   m->st.n_off = desc->n_offsets;
   memcpy(m->st.off, desc->offsets, sizeof(m->st.off));
   memcpy(m->st.w, desc->weights, sizeof(m->st.w));
+  // term table: off-centre points + the diagonal, sorted by the column offset
+  // dz*nx*ny + dy*nx + dx they produce for an interior point
+  const int nt = desc->n_offsets + 1;
+  std::vector<int4> terms(nt);
+  std::vector<double> tw(nt, 0.0);
+  std::vector<int> idx(nt);
+  auto flat = [&](int o) -> int64_t {
+    if (o == nt - 1) return 0;
+    return (int64_t)desc->offsets[o][2] * desc->nx * desc->ny + (int64_t)desc->offsets[o][1] * desc->nx +
+           desc->offsets[o][0];
+  };
+  for (int o = 0; o < nt; ++o) idx[o] = o;
+  for (int i = 1; i < nt; ++i)
+    for (int j = i; j > 0 && flat(idx[j]) < flat(idx[j - 1]); --j) std::swap(idx[j], idx[j - 1]);
+  for (int o = 0; o < nt; ++o) {
+    const int k = idx[o];
+    if (k == nt - 1) {
+      terms[o] = make_int4(0, 0, 0, 0);
+      m->center_pos = o;
+    } else {
+      terms[o] = make_int4(desc->offsets[k][0], desc->offsets[k][1], desc->offsets[k][2], (int)flat(k));
+      tw[o] = desc->weights[k];
+      m->mx |= desc->offsets[k][0] != 0;
+      m->my |= desc->offsets[k][1] != 0;
+      m->mz |= desc->offsets[k][2] != 0;
+    }
+  }
+  m->nterms = nt;
+  // shape detection: 6 face neighbours or the full 3x3x3 box, with every
+  // extent >= 3 so the lexicographic term order is the sorted one
+  {
+    bool dims_ok = desc->nx >= 3 && desc->ny >= 3 && desc->nz >= 3;
+    auto has = [&](int dx, int dy, int dz) {
+      for (int o = 0; o < desc->n_offsets; ++o)
+        if (desc->offsets[o][0] == dx && desc->offsets[o][1] == dy && desc->offsets[o][2] == dz) return true;
+      return false;
+    };
+    bool face = desc->n_offsets == 6 && has(-1, 0, 0) && has(1, 0, 0) && has(0, -1, 0) && has(0, 1, 0) &&
+                has(0, 0, -1) && has(0, 0, 1);
+    bool box = desc->n_offsets == 26;
+    for (int dz = -1; box && dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx)
+          if ((dx || dy || dz) && !has(dx, dy, dz)) box = false;
+    m->shape = !dims_ok ? SDB_SHAPE_GENERIC : (face ? SDB_SHAPE_FACE7 : (box ? SDB_SHAPE_BOX27 : SDB_SHAPE_GENERIC));
+    if (const char* env = getenv("SDB_STENCIL_GENERIC"))
+      if (atoi(env)) m->shape = SDB_SHAPE_GENERIC;
+  }
   cudaError_t e = cudaMalloc(&m->diag, sizeof(double) * n);
+  if (e == cudaSuccess) e = cudaMalloc(&m->terms, sizeof(int4) * nt);
+  if (e == cudaSuccess) e = cudaMalloc(&m->term_w, sizeof(double) * nt);
   if (e == cudaSuccess) e = cudaMemcpyAsync(m->diag, diag, sizeof(double) * n, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(m->terms, terms.data(), sizeof(int4) * nt, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(m->term_w, tw.data(), sizeof(double) * nt, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
-    int code = cuda_fail(e, "upload stencil diagonal", __FILE__, __LINE__);
+    int code = cuda_fail(e, "upload stencil", __FILE__, __LINE__);
     sdb_matrix_destroy(m);
     return code;
   }
@@ -287,6 +361,8 @@ void sdb_matrix_destroy(sdb_matrix* m) {
   if (m->colidx) cudaFree(m->colidx);
   if (m->values) cudaFree(m->values);
   if (m->diag) cudaFree(m->diag);
+  if (m->terms) cudaFree(m->terms);
+  if (m->term_w) cudaFree(m->term_w);
   delete m;
 }
 

@@ -12,6 +12,52 @@ namespace sdb {
 constexpr int kRowThreads = 256;
 constexpr int kRowWarps = kRowThreads / 32;
 
+// ---- phased-panel row schedule ------------------------------------------------
+// Block b processes, in phase t, the panel of P consecutive rows starting at
+// (t*B + b)*P.  At any moment the whole grid works on one contiguous window
+// of B*P rows, so the far neighbours of a row (e.g. +-nx*ny on a 3-D grid)
+// are touched by other blocks within a short time and hit in L2, while the
+// near neighbours (+-1, +-nx) are re-read from the block's own L1.  The
+// schedule depends only on (n, B, P): the reduction tree is fixed.
+struct PanelSched {
+  int64_t n;
+  int64_t nblocks;
+  int64_t panel;
+};
+
+// Iterate the rows of this block: calls f(base) for every block iteration
+// whose first row is base (rows base .. base+RPB-1, clipped to [.., pend)).
+template <int RPB, class F>
+__device__ __forceinline__ void for_each_panel_chunk(const PanelSched& s, F&& f) {
+  for (int64_t ph = 0;; ++ph) {
+    const int64_t p0 = (ph * s.nblocks + blockIdx.x) * s.panel;
+    if (p0 >= s.n) break;
+    const int64_t p1 = p0 + s.panel < s.n ? p0 + s.panel : s.n;
+    for (int64_t base = p0; base < p1; base += RPB) f(base, p1);
+  }
+}
+
+// Cache-policy helpers: data streamed once per pass (w_{k-1} reads, w_{k+1}
+// writes) is marked evict-first in L2 so it does not push out the gathered
+// x rows that other blocks are about to reuse.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld_d2_once(const double* ptr, uint64_t pol) {
+  double2 r;
+  asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(r.x), "=d"(r.y)
+               : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ void st_d2_once(double* ptr, double2 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(ptr), "d"(v.x),
+               "d"(v.y), "l"(pol)
+               : "memory");
+}
+
 // Sum per-thread column accumulators over every row the block touched and
 // write one partial row (ldv doubles) at partials[(slot*nblocks + block)*ldv].
 // Lanes sharing q hold the same columns: xor-shuffle them together, then add
@@ -119,11 +165,12 @@ __device__ __forceinline__ void spmv_row(const CsrView& A, int64_t row, bool val
 // its sorted place -- the storage order the CSR form of the same operator
 // would have away from the periodic wrap.
 struct StencilView {
-  int64_t nx, ny, nz;
-  int n_off;
-  int center_pos;  // offsets whose column precedes the diagonal
-  int32_t dx[26], dy[26], dz[26];
-  double w[26];
+  int nx, ny, nz;
+  int nterms;          // off-centre points + 1
+  int center_pos;      // index of the diagonal term
+  int mx, my, mz;      // does any offset move along x / y / z
+  const int4* term;    // (dx, dy, dz, interior column delta), device, nterms
+  const double* tw;    // term weights (the diagonal's comes from diag[])
   const double* diag;
 };
 
@@ -133,25 +180,18 @@ __device__ __forceinline__ void spmv_row(const StencilView& S, int64_t row, bool
 #pragma unroll
   for (int v = 0; v < VPL; ++v) y[v] = make_double2(0.0, 0.0);
   if (!valid) return;
-  const int64_t ix = row % S.nx;
-  const int64_t iy = (row / S.nx) % S.ny;
-  const int64_t iz = row / (S.nx * S.ny);
+  const int r32 = (int)row;
+  const int ix = r32 % S.nx, t = r32 / S.nx;
+  const int iy = t % S.ny, iz = t / S.ny;
   const double dg = __ldg(S.diag + row);
-  for (int o = 0; o <= S.n_off; ++o) {
-    double wt;
-    int64_t col;
-    if (o == S.center_pos) {
-      wt = dg;
-      col = row;
-    } else {
-      const int oo = o < S.center_pos ? o : o - 1;
-      int64_t jx = ix + S.dx[oo], jy = iy + S.dy[oo], jz = iz + S.dz[oo];
-      jx = jx < 0 ? jx + S.nx : (jx >= S.nx ? jx - S.nx : jx);
-      jy = jy < 0 ? jy + S.ny : (jy >= S.ny ? jy - S.ny : jy);
-      jz = jz < 0 ? jz + S.nz : (jz >= S.nz ? jz - S.nz : jz);
-      col = (jz * S.ny + jy) * S.nx + jx;
-      wt = S.w[oo];
-    }
+  for (int o = 0; o < S.nterms; ++o) {
+    const int4 tm = __ldg(S.term + o);
+    int jx = ix + tm.x, jy = iy + tm.y, jz = iz + tm.z;
+    jx = jx < 0 ? jx + S.nx : (jx >= S.nx ? jx - S.nx : jx);
+    jy = jy < 0 ? jy + S.ny : (jy >= S.ny ? jy - S.ny : jy);
+    jz = jz < 0 ? jz + S.nz : (jz >= S.nz ? jz - S.nz : jz);
+    const int64_t col = ((int64_t)jz * S.ny + jy) * S.nx + jx;
+    const double wt = (o == S.center_pos) ? dg : __ldg(S.tw + o);
     const double* xr = x + col * ldv + 2 * q;
 #pragma unroll
     for (int v = 0; v < VPL; ++v) {
@@ -162,7 +202,22 @@ __device__ __forceinline__ void spmv_row(const StencilView& S, int64_t row, bool
   }
 }
 
-StencilView make_stencil_view(const sdb_matrix* m);
+inline StencilView make_stencil_view(const sdb_matrix* m) {
+  StencilView s{};
+  s.nx = (int)m->st.nx;
+  s.ny = (int)m->st.ny;
+  s.nz = (int)m->st.nz;
+  s.nterms = m->nterms;
+  s.center_pos = m->center_pos;
+  s.mx = m->mx;
+  s.my = m->my;
+  s.mz = m->mz;
+  s.term = m->terms;
+  s.tw = m->term_w;
+  s.diag = m->diag;
+  return s;
+}
+
 inline CsrView make_csr_view(const sdb_matrix* m) { return CsrView{m->rowptr, m->colidx, m->values}; }
 
 // Instantiate F<L, VPL> for the runtime geometry.

@@ -1,0 +1,197 @@
+// Microbenchmark: what the C2 access pattern (n = 64^3 rows x 64 fp64 probes,
+// 7-point periodic gathers, w_{k+1} = 2 A w_k - w_{k-1}) can reach on B200.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 spmm_probe.cu -o spmm_probe
+// Prints one line per variant: time per launch and effective GB/s of the
+// algorithmic traffic (read w_k, read w_{k-1}, write w_{k+1}).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); return 1; } } while (0)
+
+constexpr int NX = 64, NY = 64, NZ = 64, N = NX * NY * NZ, LDV = 64;
+
+__device__ __forceinline__ double2 ldg2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ uint64_t pol_ef() { uint64_t p; asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p)); return p; }
+__device__ __forceinline__ double2 ld_once(const double* ptr, uint64_t pol) {
+  double2 r; asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(ptr), "l"(pol)); return r; }
+__device__ __forceinline__ void st_once(double* ptr, double2 v, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(ptr), "d"(v.x), "d"(v.y), "l"(pol) : "memory"); }
+
+// rows of block b: grid-wide phased panels of P rows
+template <int L, int VPL, int MODE>  // MODE 0: stream only, 1: 7-pt gathers
+__global__ void __launch_bounds__(256) step(const double* __restrict__ x, const double* prev, double* next, int P, int nb,
+                                            double* out) {
+  constexpr int RPW = 32 / L, RPB = RPW * 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / L, q = lane % L;
+  const uint64_t pol = pol_ef();
+  double acc = 0.0;
+  for (int ph = 0;; ++ph) {
+    int p0 = (ph * nb + blockIdx.x) * P;
+    if (p0 >= N) break;
+    int p1 = min(p0 + P, N);
+    for (int base = p0; base < p1; base += RPB) {
+      int row = base + warp * RPW + g;
+      if (row >= p1) continue;
+      double2 y[VPL], xi[VPL], wp[VPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        xi[v] = ldg2(x + (size_t)row * LDV + 2 * q + 2 * L * v);
+        wp[v] = ld_once(prev + (size_t)row * LDV + 2 * q + 2 * L * v, pol);
+        y[v] = make_double2(6.0 * xi[v].x, 6.0 * xi[v].y);
+      }
+      if (MODE == 1) {
+        int ix = row % NX, iy = (row / NX) % NY, iz = row / (NX * NY);
+        int cols[6] = {row - ix + (ix + NX - 1) % NX, row - ix + (ix + 1) % NX,
+                       row + (((iy + NY - 1) % NY) - iy) * NX, row + (((iy + 1) % NY) - iy) * NX,
+                       row + (((iz + NZ - 1) % NZ) - iz) * NX * NY, row + (((iz + 1) % NZ) - iz) * NX * NY};
+        double2 xv[6][VPL];
+#pragma unroll
+        for (int u = 0; u < 6; ++u)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) xv[u][v] = ldg2(x + (size_t)cols[u] * LDV + 2 * q + 2 * L * v);
+#pragma unroll
+        for (int u = 0; u < 6; ++u)
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) { y[v].x -= xv[u][v].x; y[v].y -= xv[u][v].y; }
+      }
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        double2 wn = make_double2(2.0 * 0.05 * y[v].x - wp[v].x, 2.0 * 0.05 * y[v].y - wp[v].y);
+        st_once(next + (size_t)row * LDV + 2 * q + 2 * L * v, wn, pol);
+        acc += wn.x * wn.x + wn.y * wn.y;
+      }
+    }
+  }
+  if (acc == 12345.0) out[0] = acc;
+}
+
+// Bulk-copy variant: one elected lane per warp issues cp.async.bulk of the 7
+// x rows (512 B each) of the warp's next row into a shared-memory ring, so
+// the copies are in flight without registers; the warp then consumes the
+// ring stage from shared memory.
+template <int STAGES>
+__global__ void __launch_bounds__(256) step_bulk(const double* __restrict__ x, const double* prev, double* next, int P,
+                                                 int nb, double* out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* ring = reinterpret_cast<double*>(smem_raw) + (size_t)warp * STAGES * 7 * LDV;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + 8 * STAGES * 7 * LDV * 8) + warp * STAGES;
+  const uint64_t pol = pol_ef();
+  if (lane == 0)
+    for (int s = 0; s < STAGES; ++s) {
+      uint32_t a = (uint32_t)__cvta_generic_to_shared(&bars[s]);
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(a));
+    }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+  // this warp's rows, in order
+  auto row_at = [&](int k, int& row) -> bool {
+    // k-th row of this warp across panels: each block iteration covers 8 rows (1 per warp)
+    int per_panel = (P + 7) / 8;
+    int ph = k / per_panel, it = k % per_panel;
+    int p0 = (ph * nb + blockIdx.x) * P;
+    if (p0 >= N) return false;
+    int p1 = min(p0 + P, N);
+    row = p0 + it * 8 + warp;
+    if (row >= p1) { row = -1; }
+    return true;
+  };
+  auto issue = [&](int k, int stage) {
+    int row;
+    if (!row_at(k, row) || row < 0) return;
+    if (lane == 0) {
+      int ix = row % NX, iy = (row / NX) % NY, iz = row / (NX * NY);
+      int cols[7] = {row, row - ix + (ix + NX - 1) % NX, row - ix + (ix + 1) % NX,
+                     row + (((iy + NY - 1) % NY) - iy) * NX, row + (((iy + 1) % NY) - iy) * NX,
+                     row + (((iz + NZ - 1) % NZ) - iz) * NX * NY, row + (((iz + 1) % NZ) - iz) * NX * NY};
+      uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[stage]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(7 * LDV * 8));
+      for (int u = 0; u < 7; ++u) {
+        uint32_t dst = (uint32_t)__cvta_generic_to_shared(ring + (stage * 7 + u) * LDV);
+        const double* src = x + (size_t)cols[u] * LDV;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(dst), "l"(src), "r"(LDV * 8), "r"(bar) : "memory");
+      }
+    }
+  };
+  double acc = 0.0;
+  int phase_bits = 0;
+  for (int s = 0; s < STAGES - 1; ++s) issue(s, s);
+  for (int k = 0;; ++k) {
+    int row;
+    if (!row_at(k, row)) break;
+    issue(k + STAGES - 1, (k + STAGES - 1) % STAGES);
+    if (row < 0) continue;
+    int stage = k % STAGES;
+    double2 wp = ld_once(prev + (size_t)row * LDV + 2 * lane, pol);
+    uint32_t bar = (uint32_t)__cvta_generic_to_shared(&bars[stage]);
+    uint32_t parity = (phase_bits >> stage) & 1;
+    asm volatile("{\n .reg .pred p;\n W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W;\n}" ::"r"(bar), "r"(parity) : "memory");
+    phase_bits ^= (1 << stage);
+    const double* st = ring + stage * 7 * LDV + 2 * lane;
+    double2 xi = *reinterpret_cast<const double2*>(st);
+    double2 y = make_double2(6.0 * xi.x, 6.0 * xi.y);
+#pragma unroll
+    for (int u = 1; u < 7; ++u) {
+      double2 xv = *reinterpret_cast<const double2*>(st + u * LDV);
+      y.x -= xv.x; y.y -= xv.y;
+    }
+    __syncwarp();
+    double2 wn = make_double2(0.1 * y.x - wp.x, 0.1 * y.y - wp.y);
+    st_once(next + (size_t)row * LDV + 2 * lane, wn, pol);
+    acc += wn.x * wn.x + wn.y * wn.y;
+  }
+  if (acc == 12345.0) out[0] = acc;
+}
+
+template <class F>
+float timeit(F launch, int reps) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  launch(); launch();
+  cudaEventRecord(a);
+  for (int i = 0; i < reps; ++i) launch();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  return ms / reps;
+}
+
+int main() {
+  size_t bytes = (size_t)N * LDV * 8;
+  double *x, *p, *q, *out;
+  CK(cudaMalloc(&x, bytes)); CK(cudaMalloc(&p, bytes)); CK(cudaMalloc(&q, bytes)); CK(cudaMalloc(&out, 8));
+  CK(cudaMemset(x, 0, bytes)); CK(cudaMemset(p, 0, bytes)); CK(cudaMemset(q, 0, bytes));
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const double alg = 3.0 * bytes;  // read x, read prev, write next
+  auto report = [&](const char* name, float ms) { printf("%-40s %8.1f us  %7.0f GB/s\n", name, ms * 1e3, alg / (ms * 1e-3) / 1e9); };
+  for (int bps : {2, 4, 6, 8}) {
+    int nb = bps * sms;
+    for (int P : {64, 128, 256}) {
+      char nm[128];
+      snprintf(nm, sizeof nm, "stream L32 nb=%d P=%d", nb, P);
+      report(nm, timeit([&] { step<32, 1, 0><<<nb, 256>>>(x, p, q, P, nb, out); }, 20));
+      snprintf(nm, sizeof nm, "gather7 L32 nb=%d P=%d", nb, P);
+      report(nm, timeit([&] { step<32, 1, 1><<<nb, 256>>>(x, p, q, P, nb, out); }, 20));
+      snprintf(nm, sizeof nm, "gather7 L16V2 nb=%d P=%d", nb, P);
+      report(nm, timeit([&] { step<16, 2, 1><<<nb, 256>>>(x, p, q, P, nb, out); }, 20));
+      snprintf(nm, sizeof nm, "gather7 L8V4 nb=%d P=%d", nb, P);
+      report(nm, timeit([&] { step<8, 4, 1><<<nb, 256>>>(x, p, q, P, nb, out); }, 20));
+    }
+  }
+  for (int bps : {1, 2, 3}) {
+    int nb = bps * sms;
+    for (int P : {64, 128, 256}) {
+      constexpr int ST = 4;
+      size_t sm = 8 * ST * 7 * LDV * 8 + 8 * ST * 8;
+      cudaFuncSetAttribute(step_bulk<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      char nm[128];
+      snprintf(nm, sizeof nm, "bulk4 nb=%d P=%d", nb, P);
+      report(nm, timeit([&] { step_bulk<ST><<<nb, 256, sm>>>(x, p, q, P, nb, out); }, 20));
+    }
+  }
+  CK(cudaGetLastError());
+  CK(cudaDeviceSynchronize());
+  return 0;
+}
