@@ -26,8 +26,18 @@ constexpr int kStepThreads = kRowThreads;
 constexpr int kStepWarps = kRowWarps;
 
 // Resident blocks per SM the step kernels are compiled for (register cap).
+// (compile-time tunables: -DSDB_MINB_V1=.. -DSDB_MINB_V2=.. -DSDB_U_V1=..)
+#ifndef SDB_MINB_V1
+#define SDB_MINB_V1 5
+#endif
+#ifndef SDB_MINB_V2
+#define SDB_MINB_V2 4
+#endif
+#ifndef SDB_U_V1
+#define SDB_U_V1 4
+#endif
 __host__ __device__ constexpr int step_min_blocks(int l, int vpl) {
-  return l < 8 ? (vpl == 1 ? 4 : 2) : (vpl == 1 ? 5 : (vpl == 2 ? 4 : 2));
+  return l < 8 ? (vpl == 1 ? 4 : 2) : (vpl == 1 ? SDB_MINB_V1 : (vpl == 2 ? SDB_MINB_V2 : 2));
 }
 
 struct StepArgs {
@@ -152,7 +162,7 @@ template <int L, int VPL, int MODE, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_step_csr(CsrView A, StepArgs a) {
   constexpr int RPW = 32 / L;
   constexpr int RPB = RPW * kStepWarps;
-  constexpr int U = L < 4 ? L : (VPL == 1 ? 4 : 2);
+  constexpr int U = L < 4 ? L : (VPL == 1 ? SDB_U_V1 : 2);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / L, q = lane % L;
   const uint64_t pol = policy_evict_first();
@@ -292,7 +302,7 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
   using G = GridShape<SHAPE>;
   constexpr int RPW = 32 / L;
   constexpr int RPB = RPW * kStepWarps;
-  constexpr int U = VPL == 1 ? 4 : 2;
+  constexpr int U = VPL == 1 ? SDB_U_V1 : 2;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / L, q = lane % L;
   const uint64_t pol = policy_evict_first();

@@ -145,6 +145,73 @@ __global__ void __launch_bounds__(256) step_bulk(const double* __restrict__ x, c
   if (acc == 12345.0) out[0] = acc;
 }
 
+
+// cp.async (LDGSTS, L1-allocating) software pipeline: each lane copies its own
+// 16 B columns of the 7 gathered rows + w_{k-1} of a future row iteration into
+// shared memory and later reads back exactly those bytes (no barriers).
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem) : "memory");
+}
+template <int S>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(S) : "memory"); }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+template <int STAGES>
+__global__ void __launch_bounds__(256) step_cp(const double* __restrict__ x, const double* prev, double* next, int P, int nb,
+                                               double* out) {
+  extern __shared__ __align__(16) double sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* mine = sm + (size_t)warp * STAGES * 8 * LDV + 2 * lane;  // [stage][slot][LDV]
+  const uint64_t pol = pol_ef();
+  const int per_panel = P / 8;
+  auto row_of = [&](int k) -> int {  // -2: done, -1: idle slot
+    int ph = k / per_panel, it = k % per_panel;
+    int p0 = (ph * nb + blockIdx.x) * P;
+    if (p0 >= N) return -2;
+    int row = p0 + it * 8 + warp;
+    return row < min(p0 + P, N) ? row : -1;
+  };
+  auto issue = [&](int k) {
+    int row = row_of(k);
+    double* d = mine + (k % STAGES) * 8 * LDV;
+    if (row >= 0) {
+      int ix = row % NX, iy = (row / NX) % NY, iz = row / (NX * NY);
+      int cols[7] = {row, row - ix + (ix + NX - 1) % NX, row - ix + (ix + 1) % NX,
+                     row + (((iy + NY - 1) % NY) - iy) * NX, row + (((iy + 1) % NY) - iy) * NX,
+                     row + (((iz + NZ - 1) % NZ) - iz) * NX * NY, row + (((iz + 1) % NZ) - iz) * NX * NY};
+#pragma unroll
+      for (int u = 0; u < 7; ++u) cp16(d + u * LDV, x + (size_t)cols[u] * LDV + 2 * lane);
+      cp16(d + 7 * LDV, prev + (size_t)row * LDV + 2 * lane);
+    }
+    cp_commit();
+  };
+  double acc = 0.0;
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) issue(s);
+  for (int k = 0;; ++k) {
+    int row = row_of(k);
+    if (row == -2) break;
+    issue(k + STAGES - 1);
+    cp_wait<STAGES - 1>();
+    if (row < 0) continue;
+    const double* d = mine + (k % STAGES) * 8 * LDV;
+    double2 xi = *reinterpret_cast<const double2*>(d);
+    double2 y = make_double2(6.0 * xi.x, 6.0 * xi.y);
+#pragma unroll
+    for (int u = 1; u < 7; ++u) {
+      double2 xv = *reinterpret_cast<const double2*>(d + u * LDV);
+      y.x -= xv.x; y.y -= xv.y;
+    }
+    double2 wp = *reinterpret_cast<const double2*>(d + 7 * LDV);
+    double2 wn = make_double2(0.1 * y.x - wp.x, 0.1 * y.y - wp.y);
+    st_once(next + (size_t)row * LDV + 2 * lane, wn, pol);
+    acc += wn.x * wn.x + wn.y * wn.y;
+  }
+  cp_wait<0>();
+  if (acc == 12345.0) out[0] = acc;
+}
+
 template <class F>
 float timeit(F launch, int reps) {
   cudaEvent_t a, b;
@@ -166,9 +233,9 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const double alg = 3.0 * bytes;  // read x, read prev, write next
   auto report = [&](const char* name, float ms) { printf("%-40s %8.1f us  %7.0f GB/s\n", name, ms * 1e3, alg / (ms * 1e-3) / 1e9); };
-  for (int bps : {2, 4, 6, 8}) {
+  for (int bps : {4, 6, 8}) {
     int nb = bps * sms;
-    for (int P : {64, 128, 256}) {
+    for (int P : {64}) {
       char nm[128];
       snprintf(nm, sizeof nm, "stream L32 nb=%d P=%d", nb, P);
       report(nm, timeit([&] { step<32, 1, 0><<<nb, 256>>>(x, p, q, P, nb, out); }, 20));
@@ -180,15 +247,24 @@ int main() {
       report(nm, timeit([&] { step<8, 4, 1><<<nb, 256>>>(x, p, q, P, nb, out); }, 20));
     }
   }
-  for (int bps : {1, 2, 3}) {
+  for (int bps : {2, 3, 4, 5, 6}) {
     int nb = bps * sms;
-    for (int P : {64, 128, 256}) {
-      constexpr int ST = 4;
-      size_t sm = 8 * ST * 7 * LDV * 8 + 8 * ST * 8;
-      cudaFuncSetAttribute(step_bulk<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    for (int P : {64}) {
       char nm[128];
-      snprintf(nm, sizeof nm, "bulk4 nb=%d P=%d", nb, P);
-      report(nm, timeit([&] { step_bulk<ST><<<nb, 256, sm>>>(x, p, q, P, nb, out); }, 20));
+      {
+        constexpr int ST = 2;
+        size_t sm = (size_t)8 * ST * 8 * LDV * 8;
+        cudaFuncSetAttribute(step_cp<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        snprintf(nm, sizeof nm, "cp.async ST2 nb=%d P=%d", nb, P);
+        report(nm, timeit([&] { step_cp<ST><<<nb, 256, sm>>>(x, p, q, P, nb, out); }, 20));
+      }
+      {
+        constexpr int ST = 3;
+        size_t sm = (size_t)8 * ST * 8 * LDV * 8;
+        cudaFuncSetAttribute(step_cp<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        snprintf(nm, sizeof nm, "cp.async ST3 nb=%d P=%d", nb, P);
+        report(nm, timeit([&] { step_cp<ST><<<nb, 256, sm>>>(x, p, q, P, nb, out); }, 20));
+      }
     }
   }
   CK(cudaGetLastError());
