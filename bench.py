@@ -39,7 +39,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--format", default="csr", choices=["csr", "stencil"])
+    ap.add_argument("--format", default="csr", choices=["csr", "csr-raw", "stencil"],
+                    help="csr: the config's CSR matrix through the matrix layer (stencil detection on); "
+                         "csr-raw: CSR kernel forced; stencil: StencilOperator input")
     ap.add_argument("--direct", action="store_true", help="direct (non-doubling) moments")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-probes", type=int, default=0)
@@ -121,8 +123,10 @@ def build_workload(config, fmt):
     cfg = W.CONFIGS[config]
     op = W.build_matrix(config)
     iv = W.gershgorin_interval(op)
-    if fmt == "csr" and not isinstance(op, SparseSymmetricMatrix):
+    if fmt in ("csr", "csr-raw") and not isinstance(op, SparseSymmetricMatrix):
         op = SparseSymmetricMatrix(csr=op.csr)
+    if fmt == "csr-raw":
+        os.environ["SDB_AUTO_STENCIL"] = "0"
     return cfg, op, iv
 
 
@@ -307,6 +311,8 @@ def main():
     achieved = bytes_launch / avg_launch_s / 1e9
     peak, peak_kind = load_peaks()
     traffic = load_traffic(args.config, args.format)
+    internal = ("stencil (detected from CSR)" if dm.detected_stencil else
+                ("stencil" if dm.format == _native.SDB_FMT_STENCIL else "csr"))
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic, "kernel": "cheb_step_kernel", "peak_source": f"{peak_kind} hbm_gbs",
             "bytes_per_launch": bytes_launch, "launches_per_step": launches,
@@ -326,7 +332,7 @@ def main():
         "value": value, "unit": "GNNZ-vec/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generators, paper_1308_5467_b200/workloads.py)",
-        "config": config_dict(cfg, args.format, product, op, world),
+        "config": dict(config_dict(cfg, args.format, product, op, world), internal_format=internal),
         "roofline": roof, "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "GNNZ-vec/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3,

@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
       if (row >= pend) continue;
       EpiIn<VPL> e;
       epi_load<L, VPL, MODE, FIRST>(a, row, q, pol, e);
+      const double dg = __ldg(S.diag + row);
       const int r32 = (int)row;
       const int ix = r32 % nx, t = r32 / nx;
       const int iy = t % ny, iz = t / ny;
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
             const int oy = G::dy(o) < 0 ? ym : (G::dy(o) > 0 ? yp : 0);
             const int oz = G::dz(o) < 0 ? zm : (G::dz(o) > 0 ? zp : 0);
             col[u] = r32 + ox + oy + oz;
-            w[u] = (G::dx(o) == 0 && G::dy(o) == 0 && G::dz(o) == 0) ? __ldg(S.diag + row) : __ldg(S.tw + o);
+            w[u] = (G::dx(o) == 0 && G::dy(o) == 0 && G::dz(o) == 0) ? dg : S.wc[o];
           } else {
             col[u] = r32;
             w[u] = 0.0;

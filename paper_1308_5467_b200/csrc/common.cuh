@@ -72,6 +72,7 @@ struct sdb_matrix {
   double* diag = nullptr;
   int4* terms = nullptr;      // (dx, dy, dz, interior column delta), sorted by delta
   double* term_w = nullptr;   // weight per term (diagonal slot unused)
+  double term_w_host[27] = {};
   int nterms = 0, center_pos = 0, mx = 0, my = 0, mz = 0;
   int shape = 0;              // SDB_SHAPE_*: specialised grid kernel available
 };

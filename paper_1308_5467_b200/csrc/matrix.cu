@@ -305,6 +305,7 @@ int sdb_matrix_create_stencil(int device, const sdb_stencil_desc* desc, const do
     }
   }
   m->nterms = nt;
+  for (int o = 0; o < nt; ++o) m->term_w_host[o] = tw[o];
   // shape detection: 6 face neighbours or the full 3x3x3 box, with every
   // extent >= 3 so the lexicographic term order is the sorted one
   {

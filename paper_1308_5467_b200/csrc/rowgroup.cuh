@@ -172,6 +172,8 @@ struct StencilView {
   const int4* term;    // (dx, dy, dz, interior column delta), device, nterms
   const double* tw;    // term weights (the diagonal's comes from diag[])
   const double* diag;
+  double wc[27];       // the same weights by value: compile-time indexed by the
+                       // grid kernels, read straight from the constant bank
 };
 
 template <int L, int VPL>
@@ -215,6 +217,7 @@ inline StencilView make_stencil_view(const sdb_matrix* m) {
   s.term = m->terms;
   s.tw = m->term_w;
   s.diag = m->diag;
+  for (int o = 0; o < 27; ++o) s.wc[o] = o < m->nterms ? m->term_w_host[o] : 0.0;
   return s;
 }
 

@@ -17,6 +17,7 @@ that calls the protocol directly; the engine does not use them.
 """
 
 import ctypes
+import os
 import threading
 import weakref
 from dataclasses import dataclass
@@ -297,10 +298,84 @@ def _csr_arrays(base):
     return csr, n
 
 
+def _divisors(v, lo=3):
+    out = []
+    i = 1
+    while i * i <= v:
+        if v % i == 0:
+            for d in (i, v // i):
+                if d >= lo and d not in out:
+                    out.append(d)
+        i += 1
+    return sorted(out)
+
+
+def detect_stencil(csr):
+    """Recognise a CSR that is exactly a periodic constant-coefficient stencil.
+
+    Part of the matrix layer's format selection: when every row stores the
+    same pattern of <= 27 neighbours on some nx*ny*nz torus (nx, ny, nz >= 3)
+    with one constant weight per neighbour offset, the matrix is re-expressed
+    as a ``StencilOperator`` with the CSR's own diagonal -- the identical
+    operator, whose step kernels gather neighbours by index arithmetic
+    instead of streaming column indices.  The candidate is accepted only if
+    its CSR form equals the input array for array (indices and values).
+    Returns None otherwise.
+    """
+    n = csr.shape[0]
+    if n < 27:
+        return None
+    counts = np.diff(csr.indptr)
+    k = int(counts[0])
+    if k < 2 or k > 27 or np.any(counts != k):
+        return None
+    if not csr.has_sorted_indices:
+        return None
+    cols = np.asarray(csr.indices).reshape(n, k)
+    vals = np.asarray(csr.data).reshape(n, k)
+    for nx in _divisors(n):
+        for ny in _divisors(n // nx):
+            nz = n // (nx * ny)
+            if nz < 3:
+                continue
+            r = ((nz // 2) * ny + ny // 2) * nx + nx // 2
+            d = cols[r].astype(np.int64) - r
+            offs, weights, has_diag = [], [], False
+            ok = True
+            for dd, vv in zip(d, vals[r]):
+                dz = int(np.round(dd / (nx * ny)))
+                rem = dd - dz * nx * ny
+                dy = int(np.round(rem / nx))
+                dx = int(rem - dy * nx)
+                if max(abs(dx), abs(dy), abs(dz)) > 1:
+                    ok = False
+                    break
+                if dx == dy == dz == 0:
+                    has_diag = True
+                else:
+                    offs.append((dx, dy, dz))
+                    weights.append(float(vv))
+            if not ok or not has_diag or not offs:
+                continue
+            on = cols == np.arange(n)[:, None]
+            if not np.all(on.sum(axis=1) == 1):
+                return None
+            diag = np.ascontiguousarray(vals[on], dtype=np.float64)
+            try:
+                cand = StencilOperator((nx, ny, nz), offs, weights, diag)
+            except ValueError:
+                continue
+            ref = cand.csr
+            if np.array_equal(ref.indices, csr.indices) and np.array_equal(ref.data, csr.data):
+                return cand
+    return None
+
+
 class DeviceMatrix:
     """Owns one ``sdb_matrix`` handle on one CUDA device."""
 
-    def __init__(self, handle, device, n, nnz, fmt, stream_bytes):
+    def __init__(self, handle, device, n, nnz, fmt, stream_bytes, detected=False):
+        self.detected_stencil = detected  # CSR input re-expressed as a stencil
         self.handle = handle
         self.device = device
         self.n = n
@@ -310,7 +385,9 @@ class DeviceMatrix:
         self._finalizer = weakref.finalize(self, _destroy_handle, handle)
 
     @classmethod
-    def upload(cls, base, device, stream):
+    def upload(cls, base, device, stream, auto_stencil=None):
+        if auto_stencil is None:
+            auto_stencil = auto_stencil_enabled()
         lib = _native.load()
         h = ctypes.c_void_p()
         if isinstance(base, StencilOperator):
@@ -324,6 +401,10 @@ class DeviceMatrix:
             diag = np.ascontiguousarray(base.diag, dtype=np.float64)
             _native.check(lib.sdb_matrix_create_stencil(device, ctypes.byref(desc), diag.ctypes.data,
                                                         stream, ctypes.byref(h)))
+        elif auto_stencil and (st := detect_stencil(_csr_arrays(base)[0])) is not None:
+            dm = cls.upload(st, device, stream, auto_stencil=False)
+            dm.detected_stencil = True
+            return dm
         else:
             csr, n = _csr_arrays(base)
             indptr = np.ascontiguousarray(csr.indptr, dtype=np.int64)
@@ -359,13 +440,19 @@ _cache_lock = threading.Lock()
 _cache = {}
 
 
+def auto_stencil_enabled():
+    """CSR -> stencil format selection (SDB_AUTO_STENCIL=0 disables it)."""
+    return os.environ.get("SDB_AUTO_STENCIL", "1") != "0"
+
+
 def _cache_key(base, device):
     if isinstance(base, StencilOperator):
         arr = base.diag
         return (id(base), device, arr.ctypes.data, arr.shape[0], "stencil")
     csr = base.csr if hasattr(base, "csr") else None
     if csr is not None:
-        return (id(base), device, csr.data.ctypes.data, csr.indices.ctypes.data, csr.nnz, "csr")
+        return (id(base), device, csr.data.ctypes.data, csr.indices.ctypes.data, csr.nnz, "csr",
+                auto_stencil_enabled())
     return None
 
 

@@ -192,17 +192,21 @@ def test_golden_c1_full(golden):
     _kpm_golden_case(golden, "c1_kpm", W.build_matrix("C1"))
 
 
-def test_golden_c2_subset_stencil_and_csr(golden):
+@pytest.mark.parametrize("auto", ["1", "0"])
+def test_golden_c2_subset_stencil_and_csr(golden, monkeypatch, auto):
+    monkeypatch.setenv("SDB_AUTO_STENCIL", auto)
     op = W.build_matrix("C2")
     _kpm_golden_case(golden, "c2_subset", op)  # stencil form
-    _kpm_golden_case(golden, "c2_subset", sdb.SparseSymmetricMatrix(csr=op.csr))  # CSR form
+    _kpm_golden_case(golden, "c2_subset", sdb.SparseSymmetricMatrix(csr=op.csr))  # CSR (detected or raw)
 
 
 def test_golden_c3_small(golden):
     _kpm_golden_case(golden, "c3_small", W.dft_like(20000))
 
 
-def test_golden_c5_small(golden):
+@pytest.mark.parametrize("auto", ["1", "0"])
+def test_golden_c5_small(golden, monkeypatch, auto):
+    monkeypatch.setenv("SDB_AUTO_STENCIL", auto)
     op = W.stencil27_3d(24)
     _kpm_golden_case(golden, "c5_small", op)
     _kpm_golden_case(golden, "c5_small", sdb.SparseSymmetricMatrix(csr=op.csr))
@@ -227,7 +231,8 @@ def test_oracle_parity_probe_widths(n_vec):
     assert rel_err(got.zeta, ref) <= MOMENT_RTOL
 
 
-def test_stencil_equals_csr_form():
+def test_stencil_equals_csr_form(monkeypatch):
+    monkeypatch.setenv("SDB_AUTO_STENCIL", "0")
     op = W.anderson_3d(12)
     iv = W.gershgorin_interval(op)
     src = sdb.ProbeVectorSource("rademacher", seed=1, dim=op.dim)
@@ -245,3 +250,37 @@ def test_deterministic_reruns():
     e2 = sdb.estimate_dos(op, iv, "kpm-jackson", 80, src, 64, grid_points=500, product_formula=True)
     np.testing.assert_array_equal(e1.density, e2.density)
     np.testing.assert_array_equal(e1.params["moments"], e2.params["moments"])
+
+
+def test_csr_stencil_detection():
+    from paper_1308_5467_b200.operators import detect_stencil
+
+    for op in (W.anderson_3d(8), W.anderson_3d(12), W.stencil27_3d(6)):
+        st = detect_stencil(op.csr)
+        assert st is not None and st.shape == op.shape
+        np.testing.assert_array_equal(st.diag, op.diag)
+        np.testing.assert_array_equal(st.csr.data, op.csr.data)
+    assert detect_stencil(W.build_matrix("C1").csr) is None  # Dirichlet faces: not periodic
+    assert detect_stencil(W.dft_like(3000, half_band=5, n_random=3).csr) is None
+    bad = W.anderson_3d(8).csr.copy()
+    bad.data[5] += 1e-3  # one off-diagonal differs: not constant-coefficient
+    assert detect_stencil(bad) is None
+
+
+@pytest.mark.parametrize("shape", ["face7", "box27", "generic"])
+def test_stencil_kernels_match_oracle(shape):
+    if shape == "face7":
+        op = W.anderson_3d(10)
+    elif shape == "box27":
+        op = W.stencil27_3d(7)
+    else:
+        rng = np.random.default_rng(1)
+        offs = [(1, 0, 0), (-1, 0, 0), (1, 1, 0), (-1, -1, 0), (0, 0, 1), (0, 0, -1)]
+        w = [0.3, 0.3, -0.2, -0.2, 0.5, 0.5]
+        op = sdb.StencilOperator((5, 6, 7), offs, w, rng.uniform(-1, 1, 210))
+    iv = W.gershgorin_interval(op)
+    src = sdb.ProbeVectorSource("rademacher", seed=2, dim=op.dim)
+    for n_vec in (1, 20, 32, 64, 130):
+        got = sdb.moments_via_product_formula(sdb.apply_spectral_map(op, iv), 41, src, n_vec)
+        per = O.chebyshev_moments(op.csr, iv.center, iv.halfwidth, 41, "rademacher", 2, n_vec, mode="direct")
+        assert rel_err(got.zeta, O.average_moments(per)) <= MOMENT_RTOL, (shape, n_vec)

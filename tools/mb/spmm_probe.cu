@@ -212,6 +212,106 @@ __global__ void __launch_bounds__(256) step_cp(const double* __restrict__ x, con
   if (acc == 12345.0) out[0] = acc;
 }
 
+
+// Ablation: the micro gather7 kernel with the real kernel's features added.
+//  F_DOTS  two per-column dot accumulators (doubling moments) + block partials
+//  F_WTAB  weights loaded per term from a device table (+ diagonal array)
+//  F_XI    x_i loaded separately, centre term gathered as a term
+//  F_U4    gathers issued in batches of 4 (instead of all at once)
+//  F_RLDV  runtime ldv
+enum { F_DOTS = 1, F_WTAB = 2, F_XI = 4, F_U4 = 8, F_RLDV = 16 };
+template <int L, int VPL, int F, int MINB>
+__global__ void __launch_bounds__(256, MINB) step_ab(const double* __restrict__ x, const double* prev, double* next, int P,
+                                                     int nb, double* out, const double* __restrict__ wt,
+                                                     const double* __restrict__ diag, int ldv_rt) {
+  constexpr int RPW = 32 / L, RPB = RPW * 8;
+  const int ldv = (F & F_RLDV) ? ldv_rt : LDV;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane / L, q = lane % L;
+  const uint64_t pol = pol_ef();
+  double2 accA[VPL], accB[VPL];
+  double acc = 0.0;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) accA[v] = accB[v] = make_double2(0.0, 0.0);
+  for (int ph = 0;; ++ph) {
+    int p0 = (ph * nb + blockIdx.x) * P;
+    if (p0 >= N) break;
+    int p1 = min(p0 + P, N);
+    for (int base = p0; base < p1; base += RPB) {
+      int row = base + warp * RPW + g;
+      if (row >= p1) continue;
+      double2 y[VPL], xi[VPL], wp[VPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        xi[v] = ldg2(x + (size_t)row * ldv + 2 * q + 2 * L * v);
+        wp[v] = ld_once(prev + (size_t)row * ldv + 2 * q + 2 * L * v, pol);
+        y[v] = make_double2(0.0, 0.0);
+      }
+      int ix = row % NX, iy = (row / NX) % NY, iz = row / (NX * NY);
+      int cols[7] = {row + (((iz + NZ - 1) % NZ) - iz) * NX * NY, row + (((iy + NY - 1) % NY) - iy) * NX,
+                     row - ix + (ix + NX - 1) % NX, row, row - ix + (ix + 1) % NX,
+                     row + (((iy + 1) % NY) - iy) * NX, row + (((iz + 1) % NZ) - iz) * NX * NY};
+      double w[7];
+#pragma unroll
+      for (int u = 0; u < 7; ++u) w[u] = (F & F_WTAB) ? (u == 3 ? __ldg(diag + row) : __ldg(wt + u)) : (u == 3 ? 6.0 : -1.0);
+      constexpr int U = (F & F_U4) ? 4 : 8;
+#pragma unroll
+      for (int o0 = 0; o0 < 7; o0 += U) {
+        double2 xv[U][VPL];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int o = o0 + u;
+#pragma unroll
+          for (int v = 0; v < VPL; ++v) {
+            if (o < 7 && ((F & F_XI) || o != 3))
+              xv[u][v] = ldg2(x + (size_t)cols[o < 7 ? o : 3] * ldv + 2 * q + 2 * L * v);
+            else if (o == 3)
+              xv[u][v] = xi[v];
+            else
+              xv[u][v] = make_double2(0.0, 0.0);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int o = o0 + u;
+          if (o < 7)
+#pragma unroll
+            for (int v = 0; v < VPL; ++v) {
+              y[v].x = fma(w[o], xv[u][v].x, y[v].x);
+              y[v].y = fma(w[o], xv[u][v].y, y[v].y);
+            }
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        double2 wn = make_double2(2.0 * ((y[v].x - 0.3 * xi[v].x) * 0.05) - wp[v].x,
+                                  2.0 * ((y[v].y - 0.3 * xi[v].y) * 0.05) - wp[v].y);
+        st_once(next + (size_t)row * ldv + 2 * q + 2 * L * v, wn, pol);
+        if (F & F_DOTS) {
+          accA[v].x += wn.x * wn.x; accA[v].y += wn.y * wn.y;
+          accB[v].x += wn.x * xi[v].x; accB[v].y += wn.y * xi[v].y;
+        } else {
+          acc += wn.x * wn.x + wn.y * wn.y;
+        }
+      }
+    }
+  }
+  if (F & F_DOTS) {
+    __shared__ double sm[8 * 64];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int off = L; off < 32; off <<= 1) {
+        accA[v].x += __shfl_xor_sync(~0u, accA[v].x, off); accA[v].y += __shfl_xor_sync(~0u, accA[v].y, off);
+        accB[v].x += __shfl_xor_sync(~0u, accB[v].x, off); accB[v].y += __shfl_xor_sync(~0u, accB[v].y, off);
+      }
+    if (lane < L)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) { sm[warp * 64 + 2 * (q + v * L)] = accA[v].x + accB[v].x; sm[warp * 64 + 2 * (q + v * L) + 1] = accA[v].y + accB[v].y; }
+    __syncthreads();
+    if (threadIdx.x < 64) { double s2 = 0; for (int w2 = 0; w2 < 8; ++w2) s2 += sm[w2 * 64 + threadIdx.x]; out[1 + blockIdx.x * 64 + threadIdx.x] = s2; }
+  } else if (acc == 12345.0) out[0] = acc;
+}
+
 template <class F>
 float timeit(F launch, int reps) {
   cudaEvent_t a, b;
@@ -233,40 +333,26 @@ int main() {
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const double alg = 3.0 * bytes;  // read x, read prev, write next
   auto report = [&](const char* name, float ms) { printf("%-40s %8.1f us  %7.0f GB/s\n", name, ms * 1e3, alg / (ms * 1e-3) / 1e9); };
-  for (int bps : {4, 6, 8}) {
-    int nb = bps * sms;
-    for (int P : {64}) {
-      char nm[128];
-      snprintf(nm, sizeof nm, "stream L32 nb=%d P=%d", nb, P);
-      report(nm, timeit([&] { step<32, 1, 0><<<nb, 256>>>(x, p, q, P, nb, out); }, 20));
-      snprintf(nm, sizeof nm, "gather7 L32 nb=%d P=%d", nb, P);
-      report(nm, timeit([&] { step<32, 1, 1><<<nb, 256>>>(x, p, q, P, nb, out); }, 20));
-      snprintf(nm, sizeof nm, "gather7 L16V2 nb=%d P=%d", nb, P);
-      report(nm, timeit([&] { step<16, 2, 1><<<nb, 256>>>(x, p, q, P, nb, out); }, 20));
-      snprintf(nm, sizeof nm, "gather7 L8V4 nb=%d P=%d", nb, P);
-      report(nm, timeit([&] { step<8, 4, 1><<<nb, 256>>>(x, p, q, P, nb, out); }, 20));
-    }
+  double *wt, *dg;
+  CK(cudaMalloc(&wt, 64)); CK(cudaMalloc(&dg, N * 8)); CK(cudaMemset(wt, 0, 64)); CK(cudaMemset(dg, 0, N * 8));
+  CK(cudaFree(out)); CK(cudaMalloc(&out, 8 * (1 + 2000 * 64)));
+#define AB(LL, VV, FF, MB)                                                                                    \
+  for (int bps : {4, 5, 6}) {                                                                                 \
+    int nb = bps * sms;                                                                                       \
+    char nm[128];                                                                                             \
+    snprintf(nm, sizeof nm, "ab L%d V%d F=%02d MB=%d nb=%d", LL, VV, FF, MB, nb);                             \
+    report(nm, timeit([&] { step_ab<LL, VV, FF, MB><<<nb, 256>>>(x, p, q, 64, nb, out, wt, dg, LDV); }, 20)); \
   }
-  for (int bps : {2, 3, 4, 5, 6}) {
-    int nb = bps * sms;
-    for (int P : {64}) {
-      char nm[128];
-      {
-        constexpr int ST = 2;
-        size_t sm = (size_t)8 * ST * 8 * LDV * 8;
-        cudaFuncSetAttribute(step_cp<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        snprintf(nm, sizeof nm, "cp.async ST2 nb=%d P=%d", nb, P);
-        report(nm, timeit([&] { step_cp<ST><<<nb, 256, sm>>>(x, p, q, P, nb, out); }, 20));
-      }
-      {
-        constexpr int ST = 3;
-        size_t sm = (size_t)8 * ST * 8 * LDV * 8;
-        cudaFuncSetAttribute(step_cp<ST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        snprintf(nm, sizeof nm, "cp.async ST3 nb=%d P=%d", nb, P);
-        report(nm, timeit([&] { step_cp<ST><<<nb, 256, sm>>>(x, p, q, P, nb, out); }, 20));
-      }
-    }
-  }
+  AB(32, 1, 0, 1)
+  AB(32, 1, F_DOTS, 1)
+  AB(32, 1, F_WTAB, 1)
+  AB(32, 1, F_XI, 1)
+  AB(32, 1, F_U4, 1)
+  AB(32, 1, F_RLDV, 1)
+  AB(32, 1, F_DOTS | F_WTAB | F_XI | F_U4 | F_RLDV, 1)
+  AB(32, 1, F_DOTS | F_WTAB | F_XI | F_U4 | F_RLDV, 5)
+  AB(16, 2, 0, 1)
+  AB(16, 2, F_DOTS | F_WTAB | F_XI | F_U4 | F_RLDV, 1)
   CK(cudaGetLastError());
   CK(cudaDeviceSynchronize());
   return 0;
