@@ -139,23 +139,33 @@ def nnz_of(op):
 # does not travel to the GPU box)
 
 
-def cpu_sample(op, iv, cfg, probes, product):
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_sample(op, iv, cfg, probes, product, threads):
+    """Time the C restatement of the reference recurrence (oracle/c) on the host."""
+    from oracle import c_oracle as C
     from oracle import specdens_oracle as O
 
-    csr = op.csr
+    pr = np.array([O.draw_probe(cfg.probe_kind, 0, op.dim, l) for l in range(probes)])
     t0 = time.perf_counter()
-    O.chebyshev_moments(csr, iv.center, iv.halfwidth, cfg.degree, cfg.probe_kind, 0, probes,
-                        mode="product" if product else "direct")
+    C.cheb_moments(op.csr, iv.center, iv.halfwidth, cfg.degree, pr, "doubling" if product else "direct", threads)
     return time.perf_counter() - t0
 
 
-def cpu_baseline(op, iv, cfg, product, probes):
-    secs = cpu_sample(op, iv, cfg, probes, product)
+def cpu_baseline(op, iv, cfg, product, probes=0):
+    threads = cpu_threads()
+    probes = probes or min(64, max(2, threads))
+    secs = cpu_sample(op, iv, cfg, probes, product, threads)
     gnnz = nnz_of(op) * probes * cfg.degree / secs / 1e9
-    return {"value": gnnz, "unit": "GNNZ-vec/s", "cores": 1, "kind": "port",
+    return {"value": gnnz, "unit": "GNNZ-vec/s", "cores": min(threads, probes), "kind": "port",
             "sample": f"{cfg.name}: {probes} probes x M={cfg.degree} "
-                      f"({'product formula' if product else 'direct'}), NumPy/SciPy oracle "
-                      f"(scipy csr_matvec, single thread), {secs:.2f} s"}
+                      f"({'doubling' if product else 'direct'} recurrence) of the CSR matrix, C restatement of "
+                      f"the reference (oracle/c, csr_matvec order, one probe per pthread), {secs:.2f} s wall"}
 
 
 def run_reference_arm(args):
@@ -164,10 +174,11 @@ def run_reference_arm(args):
         return
     cfg, op, iv = build_workload(args.config, "csr")
     product = not args.direct
-    probes = args.cpu_sample_probes or 2
+    threads = cpu_threads()
+    probes = args.cpu_sample_probes or min(64, max(2, threads))
     times = []
     for i in range(args.warmup + args.steps):
-        s = cpu_sample(op, iv, cfg, probes, product)
+        s = cpu_sample(op, iv, cfg, probes, product, threads)
         if i >= args.warmup:
             times.append(s)
     t = statistics.mean(times)
@@ -176,10 +187,11 @@ def run_reference_arm(args):
         "impl": "reference", "metric": "Chebyshev moment steps: nnz*n_vec*deg/s (GNNZ-vec/s)", "value": value,
         "unit": "GNNZ-vec/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_dict(cfg, "csr", product, op, args.gpus),
-        "cpu_baseline": {"value": value, "unit": "GNNZ-vec/s", "cores": 1, "kind": "port",
-                         "sample": f"each step: {probes} probes x M={cfg.degree} of {cfg.name} on the host, "
-                                   "NumPy/SciPy oracle port of the reference (single thread)"},
+        "data": "synthetic", "config": config_dict(cfg, "csr", product, op, 1),
+        "cpu_baseline": {"value": value, "unit": "GNNZ-vec/s", "cores": min(threads, probes), "kind": "port",
+                         "sample": f"each step: {probes} probes x M={cfg.degree} of {cfg.name} "
+                                   f"({'doubling' if product else 'direct'}) on {min(threads, probes)} host "
+                                   "threads, C restatement of the reference recurrence (oracle/c)"},
         "e2e": {"value": value, "unit": "GNNZ-vec/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -321,7 +333,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_baseline(op, iv, cfg, product, args.cpu_sample_probes or 4)
+            cpu = cpu_baseline(op, iv, cfg, product, args.cpu_sample_probes)
         except Exception as exc:  # the baseline must not sink the GPU line
             cpu = {"value": None, "unit": "GNNZ-vec/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
