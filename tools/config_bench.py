@@ -1,0 +1,120 @@
+"""Time every BASELINE config on one GPU (device-resident probes, CUDA events).
+
+  python tools/config_bench.py [C1 C2 C3 C4 C5] [--format csr|stencil] [--reps 3]
+
+Prints one JSON line per config: wall time of one full estimate, GNNZ-vec/s
+(nnz * n_vec * M / t), the step-kernel roofline fraction (KPM) or the whole
+Lanczos run's algorithmic-bytes rate (Lanczos).  Not the headline bench
+(bench.py measures C2); used for DESIGN.md and profiles/.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", default=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--format", default="native", choices=["native", "csr", "csr-raw"])
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    if args.format == "csr-raw":
+        os.environ["SDB_AUTO_STENCIL"] = "0"
+    import torch
+
+    import paper_1308_5467_b200 as sdb
+    from paper_1308_5467_b200 import _native
+    from paper_1308_5467_b200 import engine as E
+    from paper_1308_5467_b200 import lanczos as LZ
+    from paper_1308_5467_b200 import workloads as W
+
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    dev = 0
+    torch.cuda.set_device(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    for name in args.configs:
+        cfg = W.CONFIGS[name]
+        t0 = time.time()
+        op = W.build_matrix(name)
+        iv = W.gershgorin_interval(op)
+        if args.format != "native" and not isinstance(op, sdb.SparseSymmetricMatrix):
+            op = sdb.SparseSymmetricMatrix(csr=op.csr)
+        gen_s = time.time() - t0
+        n = op.dim
+        nnz = int(op.csr.nnz) if isinstance(op, sdb.SparseSymmetricMatrix) else int(op.nnz)
+        src = sdb.ProbeVectorSource(cfg.probe_kind, seed=0, dim=n)
+        probes = src.draw_block(0, cfg.n_vec).to(dev)
+        times, kms = [], []
+        if cfg.method == "lanczos":
+            grid = E.to_device(sdb.interval_grid(iv, cfg.grid_points), dev)
+            for r in range(args.reps + 1):
+                flush.fill_(1)
+                torch.cuda.synchronize()
+                t = time.perf_counter()
+                res, theta, tau2, sd, _ = LZ.lanczos_quadrature_device(op, cfg.degree, None, cfg.n_vec,
+                                                                       device=dev, probes=probes)
+                stream = E.stream_ptr(dev)
+                nodes, weights = LZ._pool_device(theta, tau2, sd, cfg.n_vec, dev, stream)
+                LZ._blur_device(nodes, weights, grid, "gaussian", cfg.sigma, 1.0, dev, stream)
+                torch.cuda.synchronize()
+                if r:
+                    times.append(time.perf_counter() - t)
+            dm = res.base
+            ldv = E.block_ldv(cfg.n_vec)
+            from paper_1308_5467_b200.operators import device_matrix
+
+            ma = device_matrix(res.base, dev, E.stream_ptr(dev)).bytes_per_pass
+            m = cfg.degree
+            total = sum(ma + 8 * n * ldv * (4 * (j + 1) + 11) for j in range(m))
+            minimal = sum(ma + 8 * n * ldv * (3 * (j + 1) + 3) for j in range(m))
+            t = statistics.median(times)
+            out = {"config": name, "method": "lanczos", "n": n, "nnz": nnz, "n_vec": cfg.n_vec, "steps": m,
+                   "seconds": t, "gnnz_vec_s": nnz * cfg.n_vec * m / t / 1e9,
+                   "bytes_moved_model_TB": total / 1e12, "achieved_GBs": total / t / 1e9,
+                   "frac_of_peak": total / t / 1e9 / peak, "minimal_3pass_TB": minimal / 1e12,
+                   "frac_vs_minimal_bytes": minimal / t / 1e9 / peak, "gen_s": gen_s}
+        else:
+            mode = _native.SDB_CHEB_DOUBLING
+            mapped = sdb.apply_spectral_map(op, iv)
+            grid = sdb.unit_grid(cfg.grid_points)
+            from paper_1308_5467_b200.compare import kpm_dos_device
+
+            for r in range(args.reps + 1):
+                flush.fill_(1)
+                torch.cuda.synchronize()
+                t = time.perf_counter()
+                zeta, vals, dens, nonfinite, run = kpm_dos_device(mapped, cfg.degree, None, cfg.n_vec, "jackson",
+                                                                  grid, True, device=dev, probes=probes,
+                                                                  time_steps=True)
+                torch.cuda.synchronize()
+                if r:
+                    times.append(time.perf_counter() - t)
+                    kms.append(run.step_ms)
+            t = statistics.median(times)
+            steps = (cfg.degree + 1) // 2
+            bytes_launch = run.dm.bytes_per_pass + 24 * n * cfg.n_vec
+            k = statistics.median(kms) * 1e-3
+            out = {"config": name, "method": "kpm-jackson (doubling)", "n": n, "nnz": nnz, "n_vec": cfg.n_vec,
+                   "degree": cfg.degree, "format": "stencil" if run.dm.format == _native.SDB_FMT_STENCIL else "csr",
+                   "detected_stencil": run.dm.detected_stencil, "seconds": t,
+                   "gnnz_vec_s": nnz * cfg.n_vec * cfg.degree / t / 1e9,
+                   "step_us": k / steps * 1e6, "bytes_per_step": bytes_launch,
+                   "achieved_GBs": bytes_launch / (k / steps) / 1e9,
+                   "frac_of_peak": bytes_launch / (k / steps) / 1e9 / peak, "nonfinite": bool(nonfinite),
+                   "gen_s": gen_s}
+        print(json.dumps(out), flush=True)
+        del op, probes
+        E.Workspace.release()
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
