@@ -297,6 +297,13 @@ struct GridShape<SDB_SHAPE_BOX27> {
   __host__ __device__ static constexpr int dz(int o) { return o / 9 - 1; }
 };
 
+struct GridShapeTable {
+  int nt;
+};
+inline GridShapeTable grid_shape_table(int shape) {
+  return GridShapeTable{shape == SDB_SHAPE_FACE7 ? 7 : 27};
+}
+
 template <int SHAPE, int L, int VPL, int MODE, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_step_grid(StencilView S, StepArgs a) {
   using G = GridShape<SHAPE>;
@@ -355,6 +362,8 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
   }
   step_finish<L, VPL, MODE, FIRST>(a, accA, accB, accZ);
 }
+
+#include "tile25d.cuh"
 
 // Degree 0: only zeta_0 = <v0, v0>.
 template <int L, int VPL>
@@ -501,6 +510,87 @@ static int launch_self_dot(const Geometry& g, const StepArgs& a, cudaStream_t s)
   return SDB_OK;
 }
 
+// ---- 2.5-D tile path (tile25d.cuh) ------------------------------------------------
+struct TilePlan {
+  bool on = false;
+  int CS = 8, TY = 2;
+  int slices = 0;
+  int64_t nblocks = 0;  // spatial blocks (partials rows)
+  TileArgs t{};
+  size_t smem = 0;
+};
+
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+static TilePlan plan_tile(const sdb_matrix* m, int64_t ldv, int mode) {
+  TilePlan p;
+  if (mode != SDB_CHEB_DOUBLING || m->format != SDB_FMT_STENCIL) return p;
+  if (m->shape != SDB_SHAPE_FACE7 && m->shape != SDB_SHAPE_BOX27) return p;
+  if (!env_int("SDB_TILE", 1)) return p;
+  p.CS = env_int("SDB_TILE_CS", 8);
+  p.TY = env_int("SDB_TILE_TY", 2);
+  if (!((p.CS == 8 || p.CS == 16) && (p.TY == 2 || p.TY == 4))) return p;
+  if (ldv % p.CS != 0) return p;
+  const int nx = (int)m->st.nx, ny = (int)m->st.ny, nz = (int)m->st.nz;
+  p.t.nx = nx;
+  p.t.ny = ny;
+  p.t.nz = nz;
+  p.t.TX = nx < kTileMaxX ? nx : kTileMaxX;
+  p.t.n_xt = (nx + p.t.TX - 1) / p.t.TX;
+  p.t.n_yt = (ny + p.TY - 1) / p.TY;
+  p.slices = (int)(ldv / p.CS);
+  const int64_t base = (int64_t)p.t.n_xt * p.t.n_yt * p.slices;
+  const int64_t want = 4LL * num_sms(m->device);
+  int nzs = (int)((want + base - 1) / base);
+  if (const char* e = getenv("SDB_TILE_ZSEG")) nzs = atoi(e);
+  nzs = nzs < 1 ? 1 : nzs;
+  if (nzs > nz / 4) nzs = nz / 4 > 0 ? nz / 4 : 1;
+  p.t.ZS = (nz + nzs - 1) / nzs;
+  p.t.n_zs = (nz + p.t.ZS - 1) / p.t.ZS;
+  p.t.diag = m->diag;
+  // weights in lexicographic (dz, dy, dx) order = sorted term order
+  for (int o = 0; o < 27; ++o) p.t.wc[o] = 0.0;
+  const GridShapeTable tab = grid_shape_table(m->shape);
+  for (int o = 0; o < tab.nt; ++o) p.t.wc[o] = o < m->nterms ? m->term_w_host[o] : 0.0;
+  p.nblocks = (int64_t)p.t.n_xt * p.t.n_yt * p.t.n_zs;
+  p.smem = (p.CS == 8 ? (p.TY == 2 ? TileSmem<8, 2>::bytes : TileSmem<8, 4>::bytes)
+                      : (p.TY == 2 ? TileSmem<16, 2>::bytes : TileSmem<16, 4>::bytes));
+  p.on = true;
+  return p;
+}
+
+template <int SHAPE, int CS, int TY, bool FIRST>
+static int launch_tile_t(const TilePlan& p, const StepArgs& a, cudaStream_t s) {
+  auto fn = cheb_step_tile<SHAPE, CS, TY, FIRST>;
+  static bool configured = false;  // per instantiation
+  if (!configured) {
+    SDB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileSmem<CS, TY>::bytes));
+    configured = true;
+  }
+  dim3 grid((unsigned)p.nblocks, (unsigned)p.slices);
+  fn<<<grid, kTileThreads, TileSmem<CS, TY>::bytes, s>>>(p.t, a);
+  return SDB_OK;
+}
+
+template <bool FIRST>
+static int launch_tile(const sdb_matrix* m, const TilePlan& p, const StepArgs& a, cudaStream_t s) {
+#define SDB_TILE_CASE(SH)                                                          \
+  if (p.CS == 8 && p.TY == 2) return launch_tile_t<SH, 8, 2, FIRST>(p, a, s);      \
+  if (p.CS == 8 && p.TY == 4) return launch_tile_t<SH, 8, 4, FIRST>(p, a, s);      \
+  if (p.CS == 16 && p.TY == 2) return launch_tile_t<SH, 16, 2, FIRST>(p, a, s);    \
+  if (p.CS == 16 && p.TY == 4) return launch_tile_t<SH, 16, 4, FIRST>(p, a, s);
+  if (m->shape == SDB_SHAPE_FACE7) {
+    SDB_TILE_CASE(SDB_SHAPE_FACE7)
+  } else {
+    SDB_TILE_CASE(SDB_SHAPE_BOX27)
+  }
+#undef SDB_TILE_CASE
+  return fail(SDB_EUNSUPPORTED, "no tile kernel for CS=%d TY=%d", p.CS, p.TY);
+}
+
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 static void cheb_layout(const sdb_matrix* m, int64_t ldv, int64_t degree, size_t* block_bytes,
@@ -556,7 +646,8 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
   a.n = m->n;
   a.ldv = g.ldv;
   const int rpb = (32 / g.L) * kStepWarps;
-  a.nblocks = step_blocks(m, g, rpb);
+  const TilePlan tp = plan_tile(m, g.ldv, mode);
+  a.nblocks = tp.on ? tp.nblocks : step_blocks(m, g, rpb);
   a.panel = panel_rows(m, g.ldv, rpb);
   a.partials = partials;
   StencilView st{};
@@ -586,8 +677,11 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
     if (mode == SDB_CHEB_DOUBLING) {
       a.slotB = (2 * k + 1 <= degree) ? (int)(2 * k + 1) : -1;
       a.slotA = (2 * k + 2 <= degree) ? (int)(2 * k + 2) : -1;
-      rc = k == 0 ? launch_step<SDB_CHEB_DOUBLING, true>(m, g, &st, a, s)
-                  : launch_step<SDB_CHEB_DOUBLING, false>(m, g, &st, a, s);
+      if (tp.on)
+        rc = k == 0 ? launch_tile<true>(m, tp, a, s) : launch_tile<false>(m, tp, a, s);
+      else
+        rc = k == 0 ? launch_step<SDB_CHEB_DOUBLING, true>(m, g, &st, a, s)
+                    : launch_step<SDB_CHEB_DOUBLING, false>(m, g, &st, a, s);
     } else {
       a.slotA = (int)(k + 1);
       a.slotB = -1;

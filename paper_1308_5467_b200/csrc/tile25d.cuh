@@ -1,0 +1,198 @@
+// tile25d.cuh — 2.5-D blocked Chebyshev step for periodic 7-point / 27-point
+// grids (doubling mode), included by cheb.cu after GridShape.
+//
+// Why: with 64 probes a grid point's row of the block is 512 B, so the +-ny
+// and +-nz neighbour lines do not fit in L1 and the row-panel kernel moves
+// ~3x the DRAM traffic through L2, capping it at the L2 throughput limit
+// (profiles/r01_ncu_grid_face7_c2.txt).  Here each block owns a column
+// slice (CS probes) of a TX x TY tile of the (x, y) plane and sweeps z over a
+// segment of planes.  The (TY+2) x (TX+2) halo tiles of planes z-1, z, z+1
+// sit in a 4-slot shared-memory ring; plane z+2 and w_{k-1} / diag of plane
+// z+1 are prefetched with cp.async (LDGSTS) while plane z is computed, so
+// every neighbour read is a shared-memory load and each x row crosses L2
+// about (TY+2)/TY * (ZS+2)/ZS times.
+//
+// Arithmetic per point is the grid kernel's: terms in lexicographic (dz,dy,dx)
+// order (sorted-column order), then (y - c x)/d, 2 t - w_{k-1}, store, and the
+// doubling dots <w+,w+>, <w+,w> (+ <w0,w0> on the first step).
+#pragma once
+// (included inside namespace sdb)
+
+struct TileArgs {
+  int nx, ny, nz;
+  int TX;                // tile extent in x (<= kTileMaxX)
+  int n_xt, n_yt, n_zs;  // tiles in x, y and z segments
+  int ZS;                // planes per z segment
+  int col0_stride;       // columns per slice (= CS)
+  const double* diag;
+  double wc[27];         // weights in lexicographic (dz,dy,dx) order; centre unused
+};
+
+constexpr int kTileMaxX = 64;
+constexpr int kTileThreads = 256;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16_stream(void* smem, const void* gmem) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int CS, int TY>
+struct TileSmem {
+  static constexpr int PX = kTileMaxX + 2;          // padded tile width
+  static constexpr int PLANE = (TY + 2) * PX * CS;  // doubles per plane slot
+  static constexpr int PREV = TY * kTileMaxX * CS;  // doubles per prev slot
+  static constexpr int DIAG = TY * kTileMaxX;       // doubles per diag slot
+  static constexpr size_t bytes = sizeof(double) * (4 * PLANE + 2 * PREV + 2 * DIAG);
+};
+
+template <int SHAPE, int CS, int TY, bool FIRST>
+__global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, StepArgs a) {
+  using G = GridShape<SHAPE>;
+  using SM = TileSmem<CS, TY>;
+  constexpr int L = CS / 2;                 // lanes per point (one double2 each)
+  constexpr int GROUPS = kTileThreads / L;  // points per block iteration
+  constexpr int CH = CS / 2;                // 16-byte chunks per point slice
+  extern __shared__ __align__(16) double tsm[];
+  double* planes = tsm;
+  double* prevb = tsm + 4 * SM::PLANE;
+  double* diagb = prevb + 2 * SM::PREV;
+
+  const int bid = blockIdx.x;
+  const int zs = bid % t.n_zs;
+  const int rest = bid / t.n_zs;
+  const int yt = rest % t.n_yt, xt = rest / t.n_yt;
+  const int x0 = xt * t.TX, y0 = yt * TY;
+  const int tx_n = min(t.TX, t.nx - x0), ty_n = min(TY, t.ny - y0);
+  const int zbeg = zs * t.ZS, zend = min(zbeg + t.ZS, t.nz);
+  const int col0 = blockIdx.y * CS;  // this block's probe columns [col0, col0 + CS)
+  const int tid = threadIdx.x;
+  const int g = tid / L, q = tid % L;
+  const uint64_t pol = policy_evict_first();
+  const int nx = t.nx, ny = t.ny, nz = t.nz;
+
+  auto gidx = [&](int x, int y, int z) -> int64_t {
+    x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
+    y = y < 0 ? y + ny : (y >= ny ? y - ny : y);
+    z = z < 0 ? z + nz : (z >= nz ? z - nz : z);
+    return ((int64_t)z * ny + y) * nx + x;
+  };
+  // halo tile of plane z (rows y0-1 .. y0+TY, columns x0-1 .. x0+TX) into ring slot
+  auto load_plane = [&](int z) {
+    double* dst = planes + (size_t)(z & 3) * SM::PLANE;
+    const int W = tx_n + 2, H = ty_n + 2;
+    const int total = H * W * CH;
+    for (int i = tid; i < total; i += kTileThreads) {
+      const int c = i % CH, p = i / CH;
+      const int ix = p % W, iy = p / W;
+      const int64_t row = gidx(x0 - 1 + ix, y0 - 1 + iy, z);
+      cp_async16(dst + ((size_t)iy * SM::PX + ix) * CS + 2 * c, a.x + row * a.ldv + col0 + 2 * c);
+    }
+  };
+  auto load_prev_diag = [&](int z) {
+    const int slot = z & 1;
+    double* pd = prevb + (size_t)slot * SM::PREV;
+    double* dd = diagb + (size_t)slot * SM::DIAG;
+    const int total = ty_n * tx_n * CH;
+    for (int i = tid; i < total; i += kTileThreads) {
+      const int c = i % CH, p = i / CH;
+      const int ix = p % tx_n, iy = p / tx_n;
+      const int64_t row = ((int64_t)z * ny + (y0 + iy)) * nx + (x0 + ix);
+      if (!FIRST) cp_async16_stream(pd + ((size_t)iy * kTileMaxX + ix) * CS + 2 * c, a.prev + row * a.ldv + col0 + 2 * c);
+      if (c == 0) cp_async8(dd + iy * kTileMaxX + ix, t.diag + row);
+    }
+  };
+
+  double2 accA = make_double2(0.0, 0.0), accB = accA, accZ = accA;
+  if (zbeg < zend) {
+    load_plane(zbeg - 1);
+    load_plane(zbeg);
+    load_plane(zbeg + 1);
+    load_prev_diag(zbeg);
+    cp_async_commit();
+  }
+  for (int z = zbeg; z < zend; ++z) {
+    if (z + 1 < zend) {
+      load_plane(z + 2);
+      load_prev_diag(z + 1);
+    }
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* pz[3] = {planes + (size_t)((z + 3) & 3) * SM::PLANE, planes + (size_t)(z & 3) * SM::PLANE,
+                           planes + (size_t)((z + 1) & 3) * SM::PLANE};
+    const double* pd = prevb + (size_t)(z & 1) * SM::PREV;
+    const double* dd = diagb + (size_t)(z & 1) * SM::DIAG;
+    const int npts = tx_n * ty_n;
+    for (int p = g; p < npts; p += GROUPS) {
+      const int ix = p % tx_n, iy = p / tx_n;
+      const double dg = dd[iy * kTileMaxX + ix];
+      double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int o = 0; o < G::NT; ++o) {
+        const double* src = pz[G::dz(o) + 1] +
+                            ((size_t)(iy + 1 + G::dy(o)) * SM::PX + (ix + 1 + G::dx(o))) * CS + 2 * q;
+        const double2 xv = *reinterpret_cast<const double2*>(src);
+        const double w = (G::dx(o) == 0 && G::dy(o) == 0 && G::dz(o) == 0) ? dg : t.wc[o];
+        y.x = fma(w, xv.x, y.x);
+        y.y = fma(w, xv.y, y.y);
+      }
+      const double2 xi =
+          *reinterpret_cast<const double2*>(pz[1] + ((size_t)(iy + 1) * SM::PX + (ix + 1)) * CS + 2 * q);
+      const double tx = (y.x - a.c * xi.x) * a.inv_d;
+      const double ty = (y.y - a.c * xi.y) * a.inv_d;
+      double2 wn;
+      if (FIRST) {
+        wn = make_double2(tx, ty);
+      } else {
+        const double2 wp = *reinterpret_cast<const double2*>(pd + ((size_t)iy * kTileMaxX + ix) * CS + 2 * q);
+        wn = make_double2(2.0 * tx - wp.x, 2.0 * ty - wp.y);
+      }
+      const int64_t row = ((int64_t)z * ny + (y0 + iy)) * nx + (x0 + ix);
+      st_d2_once(a.next + row * a.ldv + col0 + 2 * q, wn, pol);
+      accA.x += wn.x * wn.x;
+      accA.y += wn.y * wn.y;
+      accB.x += wn.x * xi.x;
+      accB.y += wn.y * xi.y;
+      if (FIRST) {
+        accZ.x += xi.x * xi.x;
+        accZ.y += xi.y * xi.y;
+      }
+    }
+    __syncthreads();
+  }
+  cp_async_wait<0>();
+
+  // block partials for this block's CS columns: lanes with equal q hold the
+  // same columns; sum threads in index order through shared memory.
+  __syncthreads();
+  double* red = tsm;  // reuse the ring
+  auto partial = [&](double2 v, int slot) {
+    red[tid * 2] = v.x;
+    red[tid * 2 + 1] = v.y;
+    __syncthreads();
+    if (tid < CS) {
+      const int qq = tid / 2, comp = tid % 2;
+      double s = 0.0;
+      for (int gg = 0; gg < GROUPS; ++gg) s += red[(gg * L + qq) * 2 + comp];
+      a.partials[((int64_t)slot * a.nblocks + blockIdx.x) * a.ldv + col0 + tid] = s;
+    }
+    __syncthreads();
+  };
+  if (a.slotA >= 0) partial(accA, a.slotA);
+  if (a.slotB >= 0) partial(accB, a.slotB);
+  if (FIRST && a.slot0 >= 0) partial(accZ, a.slot0);
+}
+

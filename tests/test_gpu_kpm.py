@@ -284,3 +284,37 @@ def test_stencil_kernels_match_oracle(shape):
         got = sdb.moments_via_product_formula(sdb.apply_spectral_map(op, iv), 41, src, n_vec)
         per = O.chebyshev_moments(op.csr, iv.center, iv.halfwidth, 41, "rademacher", 2, n_vec, mode="direct")
         assert rel_err(got.zeta, O.average_moments(per)) <= MOMENT_RTOL, (shape, n_vec)
+
+
+@pytest.mark.parametrize("tile", [("8", "2", "1"), ("8", "4", "3"), ("16", "2", "2"), ("16", "4", "1"), ("8", "2", "0")])
+@pytest.mark.parametrize("dims,shape", [((10, 7, 9), "face7"), ((70, 5, 6), "face7"), ((9, 6, 8), "box27"),
+                                        ((67, 3, 4), "box27")])
+def test_tile_kernel_variants_match_oracle(monkeypatch, tile, dims, shape):
+    """2.5-D tile path: slices, tile heights, z segments, partial tiles, nx > 64."""
+    cs, ty, zseg = tile
+    monkeypatch.setenv("SDB_TILE_CS", cs)
+    monkeypatch.setenv("SDB_TILE_TY", ty)
+    if zseg != "0":
+        monkeypatch.setenv("SDB_TILE_ZSEG", zseg)
+    rng = np.random.default_rng(7)
+    n = dims[0] * dims[1] * dims[2]
+    if shape == "face7":
+        offs = W.FACE_OFFSETS
+        w = list(rng.uniform(-1, 1, 3).repeat(2))
+    else:
+        offs, w = [], []
+        for o in W._positive_offsets_27():
+            v = float(rng.uniform(-1, 1))
+            offs += [o, (-o[0], -o[1], -o[2])]
+            w += [v, v]
+    op = sdb.StencilOperator(dims, offs, w, rng.uniform(-2, 2, n))
+    iv = W.gershgorin_interval(op)
+    src = sdb.ProbeVectorSource("gaussian", seed=5, dim=n)
+    per = O.chebyshev_moments(op.csr, iv.center, iv.halfwidth, 37, "gaussian", 5, 32, mode="direct")
+    ref = O.average_moments(per)
+    got = sdb.moments_via_product_formula(sdb.apply_spectral_map(op, iv), 37, src, 32)
+    assert rel_err(got.zeta, ref) <= MOMENT_RTOL
+    grid = sdb.unit_grid(300)
+    est = sdb.estimate_dos(op, iv, "kpm-jackson", 37, src, 32, grid_points=300, product_formula=True)
+    _, dens = O.evaluate_kpm_dos(O.moments_to_coefficients(ref, n, "jackson"), iv.halfwidth, grid)
+    assert np.max(np.abs(est.density - dens)) <= DOS_ATOL
