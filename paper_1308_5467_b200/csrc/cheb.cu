@@ -513,7 +513,7 @@ static int launch_self_dot(const Geometry& g, const StepArgs& a, cudaStream_t s)
 // ---- 2.5-D tile path (tile25d.cuh) ------------------------------------------------
 struct TilePlan {
   bool on = false;
-  int CS = 8, TY = 2;
+  int CS = 8, TY = 2, PD = 2;
   int slices = 0;
   int64_t nblocks = 0;  // spatial blocks (partials rows)
   TileArgs t{};
@@ -532,7 +532,8 @@ static TilePlan plan_tile(const sdb_matrix* m, int64_t ldv, int mode) {
   if (!env_int("SDB_TILE", 1)) return p;
   p.CS = env_int("SDB_TILE_CS", 8);
   p.TY = env_int("SDB_TILE_TY", 2);
-  if (!((p.CS == 8 || p.CS == 16) && (p.TY == 2 || p.TY == 4))) return p;
+  p.PD = env_int("SDB_TILE_PD", 2);
+  if (!((p.CS == 8 || p.CS == 16) && (p.TY == 2 || p.TY == 4) && (p.PD >= 1 && p.PD <= 3))) return p;
   if (ldv % p.CS != 0) return p;
   const int nx = (int)m->st.nx, ny = (int)m->st.ny, nz = (int)m->st.nz;
   p.t.nx = nx;
@@ -550,45 +551,52 @@ static TilePlan plan_tile(const sdb_matrix* m, int64_t ldv, int mode) {
   if (nzs > nz / 4) nzs = nz / 4 > 0 ? nz / 4 : 1;
   p.t.ZS = (nz + nzs - 1) / nzs;
   p.t.n_zs = (nz + p.t.ZS - 1) / p.t.ZS;
+  {
+    const size_t px = kTileMaxX + 2, R = 3 + p.PD, RP = p.PD + 1;
+    p.smem = sizeof(double) * (R * (p.TY + 2) * px * p.CS + RP * p.TY * kTileMaxX * p.CS + RP * p.TY * kTileMaxX);
+    if (p.smem > 227 * 1024) return p;  // does not fit: grid kernel instead
+  }
   p.t.diag = m->diag;
   // weights in lexicographic (dz, dy, dx) order = sorted term order
   for (int o = 0; o < 27; ++o) p.t.wc[o] = 0.0;
   const GridShapeTable tab = grid_shape_table(m->shape);
   for (int o = 0; o < tab.nt; ++o) p.t.wc[o] = o < m->nterms ? m->term_w_host[o] : 0.0;
   p.nblocks = (int64_t)p.t.n_xt * p.t.n_yt * p.t.n_zs;
-  p.smem = (p.CS == 8 ? (p.TY == 2 ? TileSmem<8, 2>::bytes : TileSmem<8, 4>::bytes)
-                      : (p.TY == 2 ? TileSmem<16, 2>::bytes : TileSmem<16, 4>::bytes));
   p.on = true;
   return p;
 }
 
-template <int SHAPE, int CS, int TY, bool FIRST>
+template <int SHAPE, int CS, int TY, int PD, bool FIRST>
 static int launch_tile_t(const TilePlan& p, const StepArgs& a, cudaStream_t s) {
-  auto fn = cheb_step_tile<SHAPE, CS, TY, FIRST>;
+  auto fn = cheb_step_tile<SHAPE, CS, TY, PD, FIRST>;
+  constexpr size_t smem = TileSmem<CS, TY, PD>::bytes;
   static bool configured = false;  // per instantiation
   if (!configured) {
-    SDB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TileSmem<CS, TY>::bytes));
+    SDB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
   dim3 grid((unsigned)p.nblocks, (unsigned)p.slices);
-  fn<<<grid, kTileThreads, TileSmem<CS, TY>::bytes, s>>>(p.t, a);
+  fn<<<grid, kTileThreads, smem, s>>>(p.t, a);
   return SDB_OK;
 }
 
 template <bool FIRST>
 static int launch_tile(const sdb_matrix* m, const TilePlan& p, const StepArgs& a, cudaStream_t s) {
-#define SDB_TILE_CASE(SH)                                                          \
-  if (p.CS == 8 && p.TY == 2) return launch_tile_t<SH, 8, 2, FIRST>(p, a, s);      \
-  if (p.CS == 8 && p.TY == 4) return launch_tile_t<SH, 8, 4, FIRST>(p, a, s);      \
-  if (p.CS == 16 && p.TY == 2) return launch_tile_t<SH, 16, 2, FIRST>(p, a, s);    \
-  if (p.CS == 16 && p.TY == 4) return launch_tile_t<SH, 16, 4, FIRST>(p, a, s);
+#define SDB_TILE_PD(SH, CS_, TY_)                                                                  \
+  if (p.CS == CS_ && p.TY == TY_) {                                                                \
+    if (p.PD == 1) return launch_tile_t<SH, CS_, TY_, 1, FIRST>(p, a, s);                          \
+    if (p.PD == 2) return launch_tile_t<SH, CS_, TY_, 2, FIRST>(p, a, s);                          \
+    if (p.PD == 3) return launch_tile_t<SH, CS_, TY_, 3, FIRST>(p, a, s);                          \
+  }
+#define SDB_TILE_CASE(SH) SDB_TILE_PD(SH, 8, 2) SDB_TILE_PD(SH, 8, 4) SDB_TILE_PD(SH, 16, 2) SDB_TILE_PD(SH, 16, 4)
   if (m->shape == SDB_SHAPE_FACE7) {
     SDB_TILE_CASE(SDB_SHAPE_FACE7)
   } else {
     SDB_TILE_CASE(SDB_SHAPE_BOX27)
   }
 #undef SDB_TILE_CASE
-  return fail(SDB_EUNSUPPORTED, "no tile kernel for CS=%d TY=%d", p.CS, p.TY);
+#undef SDB_TILE_PD
+  return fail(SDB_EUNSUPPORTED, "no tile kernel for CS=%d TY=%d PD=%d", p.CS, p.TY, p.PD);
 }
 
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }

@@ -49,26 +49,30 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-template <int CS, int TY>
+// Ring of R = 3 + PD plane slots (z-1, z, z+1 in use, PD planes in flight)
+// and PD + 1 slots for w_{k-1} / diag.
+template <int CS, int TY, int PD>
 struct TileSmem {
   static constexpr int PX = kTileMaxX + 2;          // padded tile width
+  static constexpr int R = 3 + PD;                  // plane slots
+  static constexpr int RP = PD + 1;                 // prev/diag slots
   static constexpr int PLANE = (TY + 2) * PX * CS;  // doubles per plane slot
   static constexpr int PREV = TY * kTileMaxX * CS;  // doubles per prev slot
   static constexpr int DIAG = TY * kTileMaxX;       // doubles per diag slot
-  static constexpr size_t bytes = sizeof(double) * (4 * PLANE + 2 * PREV + 2 * DIAG);
+  static constexpr size_t bytes = sizeof(double) * (R * PLANE + RP * PREV + RP * DIAG);
 };
 
-template <int SHAPE, int CS, int TY, bool FIRST>
+template <int SHAPE, int CS, int TY, int PD, bool FIRST>
 __global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, StepArgs a) {
   using G = GridShape<SHAPE>;
-  using SM = TileSmem<CS, TY>;
+  using SM = TileSmem<CS, TY, PD>;
   constexpr int L = CS / 2;                 // lanes per point (one double2 each)
   constexpr int GROUPS = kTileThreads / L;  // points per block iteration
   constexpr int CH = CS / 2;                // 16-byte chunks per point slice
   extern __shared__ __align__(16) double tsm[];
   double* planes = tsm;
-  double* prevb = tsm + 4 * SM::PLANE;
-  double* diagb = prevb + 2 * SM::PREV;
+  double* prevb = tsm + SM::R * SM::PLANE;
+  double* diagb = prevb + SM::RP * SM::PREV;
 
   const int bid = blockIdx.x;
   const int zs = bid % t.n_zs;
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, St
   };
   // halo tile of plane z (rows y0-1 .. y0+TY, columns x0-1 .. x0+TX) into ring slot
   auto load_plane = [&](int z) {
-    double* dst = planes + (size_t)(z & 3) * SM::PLANE;
+    double* dst = planes + (size_t)(((z % SM::R) + SM::R) % SM::R) * SM::PLANE;
     const int W = tx_n + 2, H = ty_n + 2;
     const int total = H * W * CH;
     for (int i = tid; i < total; i += kTileThreads) {
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, St
     }
   };
   auto load_prev_diag = [&](int z) {
-    const int slot = z & 1;
+    const int slot = z % SM::RP;
     double* pd = prevb + (size_t)slot * SM::PREV;
     double* dd = diagb + (size_t)slot * SM::DIAG;
     const int total = ty_n * tx_n * CH;
@@ -116,25 +120,35 @@ __global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, St
   };
 
   double2 accA = make_double2(0.0, 0.0), accB = accA, accZ = accA;
+  // prologue: planes zbeg-1 .. zbeg+1 and prev/diag of zbeg (group 0), then
+  // PD-1 more groups so PD groups are in flight when plane zbeg is computed
   if (zbeg < zend) {
     load_plane(zbeg - 1);
     load_plane(zbeg);
     load_plane(zbeg + 1);
     load_prev_diag(zbeg);
+  }
+  cp_async_commit();
+  for (int j = 1; j < PD; ++j) {
+    if (zbeg + j < zend) {
+      load_plane(zbeg + 1 + j);
+      load_prev_diag(zbeg + j);
+    }
     cp_async_commit();
   }
   for (int z = zbeg; z < zend; ++z) {
-    if (z + 1 < zend) {
-      load_plane(z + 2);
-      load_prev_diag(z + 1);
+    // group for plane z+PD (+1 halo) and prev/diag of plane z+PD
+    if (z + PD < zend) {
+      load_plane(z + PD + 1);
+      load_prev_diag(z + PD);
     }
     cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<PD>();
     __syncthreads();
-    const double* pz[3] = {planes + (size_t)((z + 3) & 3) * SM::PLANE, planes + (size_t)(z & 3) * SM::PLANE,
-                           planes + (size_t)((z + 1) & 3) * SM::PLANE};
-    const double* pd = prevb + (size_t)(z & 1) * SM::PREV;
-    const double* dd = diagb + (size_t)(z & 1) * SM::DIAG;
+    const double* pz[3] = {planes + (size_t)((z - 1 + SM::R) % SM::R) * SM::PLANE,
+                           planes + (size_t)(z % SM::R) * SM::PLANE, planes + (size_t)((z + 1) % SM::R) * SM::PLANE};
+    const double* pd = prevb + (size_t)(z % SM::RP) * SM::PREV;
+    const double* dd = diagb + (size_t)(z % SM::RP) * SM::DIAG;
     const int npts = tx_n * ty_n;
     for (int p = g; p < npts; p += GROUPS) {
       const int ix = p % tx_n, iy = p / tx_n;
