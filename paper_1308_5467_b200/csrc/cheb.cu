@@ -529,10 +529,14 @@ static TilePlan plan_tile(const sdb_matrix* m, int64_t ldv, int mode) {
   TilePlan p;
   if (mode != SDB_CHEB_DOUBLING || m->format != SDB_FMT_STENCIL) return p;
   if (m->shape != SDB_SHAPE_FACE7 && m->shape != SDB_SHAPE_BOX27) return p;
-  if (!env_int("SDB_TILE", 1)) return p;
-  p.CS = env_int("SDB_TILE_CS", 8);
+  // Measured (profiles/r01_tile_sweep.txt): the tile path wins for the
+  // 27-point box (C5: 8.8 -> 4.8 ms/step) but not for the 7-point star at 64
+  // probes, where the row-panel grid kernel is faster; SDB_TILE=1 forces it.
+  const int dflt = m->shape == SDB_SHAPE_BOX27 ? 1 : 0;
+  if (!env_int("SDB_TILE", dflt)) return p;
+  p.CS = env_int("SDB_TILE_CS", ldv % 16 == 0 ? 16 : 8);
   p.TY = env_int("SDB_TILE_TY", 2);
-  p.PD = env_int("SDB_TILE_PD", 2);
+  p.PD = env_int("SDB_TILE_PD", 1);
   if (!((p.CS == 8 || p.CS == 16) && (p.TY == 2 || p.TY == 4) && (p.PD >= 1 && p.PD <= 3))) return p;
   if (ldv % p.CS != 0) return p;
   const int nx = (int)m->st.nx, ny = (int)m->st.ny, nz = (int)m->st.nz;
@@ -543,6 +547,7 @@ static TilePlan plan_tile(const sdb_matrix* m, int64_t ldv, int mode) {
   p.t.n_xt = (nx + p.t.TX - 1) / p.t.TX;
   p.t.n_yt = (ny + p.TY - 1) / p.TY;
   p.slices = (int)(ldv / p.CS);
+  p.t.slices = p.slices;
   const int64_t base = (int64_t)p.t.n_xt * p.t.n_yt * p.slices;
   const int64_t want = 4LL * num_sms(m->device);
   int nzs = (int)((want + base - 1) / base);
@@ -575,7 +580,7 @@ static int launch_tile_t(const TilePlan& p, const StepArgs& a, cudaStream_t s) {
     SDB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
-  dim3 grid((unsigned)p.nblocks, (unsigned)p.slices);
+  dim3 grid((unsigned)(p.nblocks * p.slices));
   fn<<<grid, kTileThreads, smem, s>>>(p.t, a);
   return SDB_OK;
 }

@@ -23,7 +23,7 @@ struct TileArgs {
   int TX;                // tile extent in x (<= kTileMaxX)
   int n_xt, n_yt, n_zs;  // tiles in x, y and z segments
   int ZS;                // planes per z segment
-  int col0_stride;       // columns per slice (= CS)
+  int slices;            // column slices (ldv / CS)
   const double* diag;
   double wc[27];         // weights in lexicographic (dz,dy,dx) order; centre unused
 };
@@ -74,50 +74,97 @@ __global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, St
   double* prevb = tsm + SM::R * SM::PLANE;
   double* diagb = prevb + SM::RP * SM::PREV;
 
-  const int bid = blockIdx.x;
+  // slice fastest: the CS-column slices of one tile run side by side, so each
+  // x row is fetched from DRAM once and its other slices hit in L2
+  const int bid = blockIdx.x / t.slices;
   const int zs = bid % t.n_zs;
   const int rest = bid / t.n_zs;
   const int yt = rest % t.n_yt, xt = rest / t.n_yt;
   const int x0 = xt * t.TX, y0 = yt * TY;
   const int tx_n = min(t.TX, t.nx - x0), ty_n = min(TY, t.ny - y0);
   const int zbeg = zs * t.ZS, zend = min(zbeg + t.ZS, t.nz);
-  const int col0 = blockIdx.y * CS;  // this block's probe columns [col0, col0 + CS)
+  const int col0 = (blockIdx.x % t.slices) * CS;  // this block's probe columns [col0, col0 + CS)
   const int tid = threadIdx.x;
   const int g = tid / L, q = tid % L;
   const uint64_t pol = policy_evict_first();
   const int nx = t.nx, ny = t.ny, nz = t.nz;
 
-  auto gidx = [&](int x, int y, int z) -> int64_t {
-    x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
-    y = y < 0 ? y + ny : (y >= ny ? y - ny : y);
-    z = z < 0 ? z + nz : (z >= nz ? z - nz : z);
-    return ((int64_t)z * ny + y) * nx + x;
-  };
-  // halo tile of plane z (rows y0-1 .. y0+TY, columns x0-1 .. x0+TX) into ring slot
-  auto load_plane = [&](int z) {
-    double* dst = planes + (size_t)(((z % SM::R) + SM::R) % SM::R) * SM::PLANE;
+  // Per-thread copy tables, built once: each plane / prev copy is then one
+  // address IMAD + one cp.async per 16-byte chunk.
+  constexpr int NCH = ((TY + 2) * SM::PX * CH + kTileThreads - 1) / kTileThreads;  // plane chunks / thread
+  constexpr int NPC = (TY * kTileMaxX * CH + kTileThreads - 1) / kTileThreads;     // prev chunks / thread
+  constexpr int NPT = (TY * kTileMaxX + GROUPS - 1) / GROUPS;                       // points / thread
+  const int64_t plane_rows = (int64_t)nx * ny;
+  int pl_smem[NCH], pl_row[NCH];
+  {
     const int W = tx_n + 2, H = ty_n + 2;
-    const int total = H * W * CH;
-    for (int i = tid; i < total; i += kTileThreads) {
-      const int c = i % CH, p = i / CH;
-      const int ix = p % W, iy = p / W;
-      const int64_t row = gidx(x0 - 1 + ix, y0 - 1 + iy, z);
-      cp_async16(dst + ((size_t)iy * SM::PX + ix) * CS + 2 * c, a.x + row * a.ldv + col0 + 2 * c);
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) {
+      const int i = tid + k * kTileThreads;
+      pl_smem[k] = -1;
+      pl_row[k] = 0;
+      if (i < H * W * CH) {
+        const int c = i % CH, p = i / CH;
+        const int ix = p % W, iy = p / W;
+        int x = x0 - 1 + ix, y = y0 - 1 + iy;
+        x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
+        y = y < 0 ? y + ny : (y >= ny ? y - ny : y);
+        pl_smem[k] = (iy * SM::PX + ix) * CS + 2 * c;
+        pl_row[k] = (y * nx + x) * (int)(a.ldv / 2) + c;  // in 16-byte units within the plane
+      }
     }
+  }
+  int pv_smem[NPC], pv_row[NPC];
+#pragma unroll
+  for (int k = 0; k < NPC; ++k) {
+    const int i = tid + k * kTileThreads;
+    pv_smem[k] = -1;
+    pv_row[k] = 0;
+    if (i < ty_n * tx_n * CH) {
+      const int c = i % CH, p = i / CH;
+      const int ix = p % tx_n, iy = p / tx_n;
+      pv_smem[k] = (iy * kTileMaxX + ix) * CS + 2 * c;
+      pv_row[k] = ((y0 + iy) * nx + (x0 + ix)) * (int)(a.ldv / 2) + c;
+    }
+  }
+  const double2* xg = reinterpret_cast<const double2*>(a.x + col0);
+  const double2* pg = reinterpret_cast<const double2*>(a.prev + col0);
+  const int64_t plane_units = plane_rows * (a.ldv / 2);  // 16-byte units per plane
+  auto load_plane = [&](int z) {
+    z = z < 0 ? z + nz : (z >= nz ? z - nz : z);
+    double* dst = planes + (size_t)(((z % SM::R) + SM::R) % SM::R) * SM::PLANE;
+    const double2* src = xg + (int64_t)z * plane_units;
+#pragma unroll
+    for (int k = 0; k < NCH; ++k)
+      if (pl_smem[k] >= 0) cp_async16(dst + pl_smem[k], src + pl_row[k]);
   };
   auto load_prev_diag = [&](int z) {
     const int slot = z % SM::RP;
     double* pd = prevb + (size_t)slot * SM::PREV;
     double* dd = diagb + (size_t)slot * SM::DIAG;
-    const int total = ty_n * tx_n * CH;
-    for (int i = tid; i < total; i += kTileThreads) {
-      const int c = i % CH, p = i / CH;
+    if (!FIRST) {
+      const double2* src = pg + (int64_t)z * plane_units;
+#pragma unroll
+      for (int k = 0; k < NPC; ++k)
+        if (pv_smem[k] >= 0) cp_async16_stream(pd + pv_smem[k], src + pv_row[k]);
+    }
+    for (int p = tid; p < ty_n * tx_n; p += kTileThreads) {
       const int ix = p % tx_n, iy = p / tx_n;
-      const int64_t row = ((int64_t)z * ny + (y0 + iy)) * nx + (x0 + ix);
-      if (!FIRST) cp_async16_stream(pd + ((size_t)iy * kTileMaxX + ix) * CS + 2 * c, a.prev + row * a.ldv + col0 + 2 * c);
-      if (c == 0) cp_async8(dd + iy * kTileMaxX + ix, t.diag + row);
+      cp_async8(dd + iy * kTileMaxX + ix, t.diag + (int64_t)z * plane_rows + (y0 + iy) * nx + (x0 + ix));
     }
   };
+  // this thread's points of a plane
+  int pt_ix[NPT], pt_iy[NPT];
+#pragma unroll
+  for (int k = 0; k < NPT; ++k) {
+    const int p = g + k * GROUPS;
+    pt_ix[k] = -1;
+    pt_iy[k] = 0;
+    if (p < tx_n * ty_n) {
+      pt_ix[k] = p % tx_n;
+      pt_iy[k] = p / tx_n;
+    }
+  }
 
   double2 accA = make_double2(0.0, 0.0), accB = accA, accZ = accA;
   // prologue: planes zbeg-1 .. zbeg+1 and prev/diag of zbeg (group 0), then
@@ -149,9 +196,10 @@ __global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, St
                            planes + (size_t)(z % SM::R) * SM::PLANE, planes + (size_t)((z + 1) % SM::R) * SM::PLANE};
     const double* pd = prevb + (size_t)(z % SM::RP) * SM::PREV;
     const double* dd = diagb + (size_t)(z % SM::RP) * SM::DIAG;
-    const int npts = tx_n * ty_n;
-    for (int p = g; p < npts; p += GROUPS) {
-      const int ix = p % tx_n, iy = p / tx_n;
+#pragma unroll
+    for (int k = 0; k < NPT; ++k) {
+      const int ix = pt_ix[k], iy = pt_iy[k];
+      if (ix < 0) continue;
       const double dg = dd[iy * kTileMaxX + ix];
       double2 y = make_double2(0.0, 0.0);
 #pragma unroll
@@ -174,7 +222,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, St
         const double2 wp = *reinterpret_cast<const double2*>(pd + ((size_t)iy * kTileMaxX + ix) * CS + 2 * q);
         wn = make_double2(2.0 * tx - wp.x, 2.0 * ty - wp.y);
       }
-      const int64_t row = ((int64_t)z * ny + (y0 + iy)) * nx + (x0 + ix);
+      const int64_t row = (int64_t)z * plane_rows + (y0 + iy) * nx + (x0 + ix);
       st_d2_once(a.next + row * a.ldv + col0 + 2 * q, wn, pol);
       accA.x += wn.x * wn.x;
       accA.y += wn.y * wn.y;
@@ -201,7 +249,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, St
       const int qq = tid / 2, comp = tid % 2;
       double s = 0.0;
       for (int gg = 0; gg < GROUPS; ++gg) s += red[(gg * L + qq) * 2 + comp];
-      a.partials[((int64_t)slot * a.nblocks + blockIdx.x) * a.ldv + col0 + tid] = s;
+      a.partials[((int64_t)slot * a.nblocks + bid) * a.ldv + col0 + tid] = s;
     }
     __syncthreads();
   };
