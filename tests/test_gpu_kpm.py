@@ -286,12 +286,15 @@ def test_stencil_kernels_match_oracle(shape):
         assert rel_err(got.zeta, O.average_moments(per)) <= MOMENT_RTOL, (shape, n_vec)
 
 
-@pytest.mark.parametrize("tile", [("8", "2", "1"), ("8", "4", "3"), ("16", "2", "2"), ("16", "4", "1"), ("8", "2", "0")])
+@pytest.mark.parametrize("tile", [("8", "2", "1", "1"), ("8", "4", "3", "2"), ("16", "2", "2", "1"),
+                                  ("16", "4", "1", "1"), ("8", "2", "0", "3")])
 @pytest.mark.parametrize("dims,shape", [((10, 7, 9), "face7"), ((70, 5, 6), "face7"), ((9, 6, 8), "box27"),
                                         ((67, 3, 4), "box27")])
 def test_tile_kernel_variants_match_oracle(monkeypatch, tile, dims, shape):
     """2.5-D tile path: slices, tile heights, z segments, partial tiles, nx > 64."""
-    cs, ty, zseg = tile
+    cs, ty, zseg, pd = tile
+    monkeypatch.setenv("SDB_TILE", "1")
+    monkeypatch.setenv("SDB_TILE_PD", pd)
     monkeypatch.setenv("SDB_TILE_CS", cs)
     monkeypatch.setenv("SDB_TILE_TY", ty)
     if zseg != "0":
