@@ -55,6 +55,7 @@ struct StepArgs {
   int slotA;           // doubling: <w+,w+>, direct: <v0,w+>   (-1: none)
   int slotB;           // doubling: <w+,w>                       (-1: none)
   int slot0;           // step 0: <w0,w0>                        (-1: none)
+  int slices;          // column slices per panel (grid kernel; 1 = whole rows)
 };
 
 // Epilogue shared by the CSR and stencil steps, split in two so the row's own
@@ -305,8 +306,17 @@ inline GridShapeTable grid_shape_table(int shape) {
 }
 
 template <int SHAPE, int L, int VPL, int MODE, bool FIRST>
-__global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_step_grid(StencilView S, StepArgs a) {
+__global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_step_grid(StencilView S, StepArgs a0) {
   using G = GridShape<SHAPE>;
+  // column slices of one panel are adjacent blocks (slice fastest)
+  const int slice = blockIdx.x % a0.slices;
+  const int64_t sb = blockIdx.x / a0.slices;
+  const int cs = (int)(a0.ldv / a0.slices);
+  StepArgs a = a0;
+  a.x += slice * cs;
+  a.prev += slice * cs;
+  a.next += slice * cs;
+  a.v0 += slice * cs;
   constexpr int RPW = 32 / L;
   constexpr int RPB = RPW * kStepWarps;
   constexpr int U = VPL == 1 ? SDB_U_V1 : 2;
@@ -318,7 +328,7 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
 #pragma unroll
   for (int v = 0; v < VPL; ++v) accA[v] = accB[v] = accZ[v] = make_double2(0.0, 0.0);
   for (int64_t ph = 0;; ++ph) {
-    const int64_t p0 = (ph * a.nblocks + blockIdx.x) * a.panel;
+    const int64_t p0 = (ph * a.nblocks + sb) * a.panel;
     if (p0 >= a.n) break;
     const int64_t pend = p0 + a.panel < a.n ? p0 + a.panel : a.n;
     for (int64_t base = p0; base < pend; base += RPB) {
@@ -360,7 +370,21 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
       epi_finish<L, VPL, MODE, FIRST>(a, row, q, y, e, accA, accB, accZ, pol);
     }
   }
-  step_finish<L, VPL, MODE, FIRST>(a, accA, accB, accZ);
+  if (a0.slices == 1) {
+    step_finish<L, VPL, MODE, FIRST>(a, accA, accB, accZ);
+  } else {
+    __shared__ double smem[kStepWarps * SDB_MAX_BATCH];
+    auto part = [&](double2 (&acc)[VPL], int slot) {
+      block_partial_cols<L, VPL>(acc, smem, a0.partials, slot, a0.nblocks, a0.ldv, sb, slice * cs, cs);
+    };
+    if (a.slotA >= 0) part(accA, a.slotA);
+    if constexpr (MODE == SDB_CHEB_DOUBLING) {
+      if (a.slotB >= 0) part(accB, a.slotB);
+    }
+    if constexpr (FIRST) {
+      if (a.slot0 >= 0) part(accZ, a.slot0);
+    }
+  }
 }
 
 #include "tile25d.cuh"
@@ -419,7 +443,7 @@ __global__ void moments_mean_kernel(const double* __restrict__ zeta_pp, int64_t 
 template <int MODE, bool FIRST>
 static int launch_step(const sdb_matrix* m, const Geometry& g, const StencilView* st, const StepArgs& a,
                        cudaStream_t s) {
-  dim3 grid((unsigned)a.nblocks), block(kStepThreads);
+  dim3 grid((unsigned)(a.nblocks * a.slices)), block(kStepThreads);
   if (m->format == SDB_FMT_CSR) {
     const CsrView A = make_csr_view(m);
 #define SDB_STEP_CASE(LL, VV) cheb_step_csr<LL, VV, MODE, FIRST><<<grid, block, 0, s>>>(A, a)
@@ -660,8 +684,22 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
   a.ldv = g.ldv;
   const int rpb = (32 / g.L) * kStepWarps;
   const TilePlan tp = plan_tile(m, g.ldv, mode);
-  a.nblocks = tp.on ? tp.nblocks : step_blocks(m, g, rpb);
-  a.panel = panel_rows(m, g.ldv, rpb);
+  a.slices = 1;
+  Geometry gk = g;  // geometry of the launched step kernel (per column slice)
+  if (!tp.on && m->format == SDB_FMT_STENCIL && (m->shape == SDB_SHAPE_FACE7 || m->shape == SDB_SHAPE_BOX27)) {
+    const int sl = env_int("SDB_GRID_SLICES", 1);
+    if (sl > 1 && g.ldv % (2 * sl) == 0) {
+      Geometry gs = choose_geometry(g.ldv / sl);
+      if (gs.ldv == g.ldv / sl) {
+        a.slices = sl;
+        gk = gs;
+      }
+    }
+  }
+  const int rpbk = (32 / gk.L) * kStepWarps;
+  a.nblocks = tp.on ? tp.nblocks : step_blocks(m, gk, rpbk) / a.slices;
+  if (a.nblocks < 1) a.nblocks = 1;
+  a.panel = panel_rows(m, g.ldv, rpbk);
   a.partials = partials;
   StencilView st{};
   if (m->format == SDB_FMT_STENCIL) st = make_stencil_view(m);
@@ -693,13 +731,13 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
       if (tp.on)
         rc = k == 0 ? launch_tile<true>(m, tp, a, s) : launch_tile<false>(m, tp, a, s);
       else
-        rc = k == 0 ? launch_step<SDB_CHEB_DOUBLING, true>(m, g, &st, a, s)
-                    : launch_step<SDB_CHEB_DOUBLING, false>(m, g, &st, a, s);
+        rc = k == 0 ? launch_step<SDB_CHEB_DOUBLING, true>(m, gk, &st, a, s)
+                    : launch_step<SDB_CHEB_DOUBLING, false>(m, gk, &st, a, s);
     } else {
       a.slotA = (int)(k + 1);
       a.slotB = -1;
-      rc = k == 0 ? launch_step<SDB_CHEB_DIRECT, true>(m, g, &st, a, s)
-                  : launch_step<SDB_CHEB_DIRECT, false>(m, g, &st, a, s);
+      rc = k == 0 ? launch_step<SDB_CHEB_DIRECT, true>(m, gk, &st, a, s)
+                  : launch_step<SDB_CHEB_DIRECT, false>(m, gk, &st, a, s);
     }
     if (rc) return rc;
     SDB_CHECK_LAUNCH();

@@ -93,6 +93,37 @@ __device__ __forceinline__ void block_partial(double2 (&acc)[VPL], double* smem,
   __syncthreads();
 }
 
+// Same, for a block that owns columns [col0, col0 + ncols) of row `bidx`.
+template <int L, int VPL>
+__device__ __forceinline__ void block_partial_cols(double2 (&acc)[VPL], double* smem, double* partials, int64_t slot,
+                                                   int64_t nblocks, int64_t ldv, int64_t bidx, int col0, int ncols) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, q = lane % L;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) {
+#pragma unroll
+    for (int off = L; off < 32; off <<= 1) {
+      acc[v].x += __shfl_xor_sync(0xffffffffu, acc[v].x, off);
+      acc[v].y += __shfl_xor_sync(0xffffffffu, acc[v].y, off);
+    }
+  }
+  if (lane < L) {
+#pragma unroll
+    for (int v = 0; v < VPL; ++v) {
+      int col = 2 * (q + v * L);
+      smem[warp * ncols + col] = acc[v].x;
+      smem[warp * ncols + col + 1] = acc[v].y;
+    }
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < ncols; col += blockDim.x) {
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kRowWarps; ++w) s += smem[w * ncols + col];
+    partials[(slot * nblocks + bidx) * ldv + col0 + col] = s;
+  }
+  __syncthreads();
+}
+
 // Sum one partial slot over blocks in block order.
 __device__ __forceinline__ double sum_blocks(const double* __restrict__ partials, int64_t slot, int64_t nblocks,
                                              int64_t ldv, int64_t l) {
