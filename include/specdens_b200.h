@@ -93,12 +93,18 @@ typedef struct sdb_matrix_info {
 
 /* Constant-coefficient stencil on a periodic 3-D grid (nx fastest):
  *   (A x)_p = diag[p] * x_p + sum_o weight[o] * x_{p + offset[o]}
- * offsets are (dx,dy,dz) triples in [-1,1]; the centre is carried by diag. */
+ * offsets are (dx,dy,dz) triples in [-1,1]; the centre is carried by diag.
+ * z_ghost = 1 makes the operator a z-slab of a larger grid (row partition):
+ * z is not wrapped; the neighbours of plane 0 / nz-1 are read from ghost
+ * planes the caller stores immediately before / after the slab's rows in
+ * every block passed as x (i.e. at x - nx*ny*ldv and x + nz*nx*ny*ldv). */
 typedef struct sdb_stencil_desc {
     int64_t nx, ny, nz;
     int32_t n_offsets;          /* <= 26 off-centre points                  */
     int32_t offsets[26][3];
     double weights[26];
+    int32_t z_ghost;
+    int32_t reserved;
 } sdb_stencil_desc;
 
 /* ---- library ----------------------------------------------------------- */
@@ -143,6 +149,18 @@ SDB_API int sdb_cheb_workspace_size(const sdb_matrix* m, int64_t n_vec, int64_t 
 SDB_API int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree,
                      int mode, const double* probes, double* zeta_pp, void* workspace,
                      size_t workspace_bytes, void* stream, float* step_ms);
+/* Step-level form of sdb_cheb_moments for callers that exchange data between
+ * steps (row-partitioned multi-GPU: halo planes).  Step k reads x = w_k,
+ * prev = w_{k-1} (k >= 1), v0 (direct mode), writes next = w_{k+1} (may alias
+ * prev) and its moment partials; sdb_cheb_reduce turns the partials of all
+ * steps into per-probe moments (linear in the rows, so per-rank results of a
+ * row partition add up).  degree = 0: step 0 only computes zeta_0. */
+SDB_API int sdb_cheb_partials_size(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode, size_t* bytes);
+SDB_API int sdb_cheb_step(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode,
+                  int64_t k, const double* x, const double* prev, double* next, const double* v0,
+                  double* partials, size_t partial_bytes, void* stream);
+SDB_API int sdb_cheb_reduce(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode, const double* partials,
+                    double* zeta_pp, void* stream);
 /* zeta[k] = (1/n_vec) sum_l zeta_pp[l][k], probes summed in index order
  * (kpm.py:135, :193).  nonfinite (device int32, may be NULL) is set to 1 if
  * any zeta[k] is not finite. */

@@ -54,6 +54,8 @@ class SdbStencilDesc(ctypes.Structure):
         ("n_offsets", ctypes.c_int32),
         ("offsets", (ctypes.c_int32 * 3) * 26),
         ("weights", ctypes.c_double * 26),
+        ("z_ghost", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 
@@ -77,6 +79,9 @@ SIGNATURES = {
     "sdb_unpack_block": (_i, [_p, _i64, _i64, _i64, _p, _p]),
     "sdb_cheb_workspace_size": (_i, [_p, _i64, _i64, _i, ctypes.POINTER(_sz)]),
     "sdb_cheb_moments": (_i, [_p, _d, _d, _i64, _i64, _i, _p, _p, _p, _sz, _p, ctypes.POINTER(ctypes.c_float)]),
+    "sdb_cheb_partials_size": (_i, [_p, _i64, _i64, _i, ctypes.POINTER(_sz)]),
+    "sdb_cheb_step": (_i, [_p, _d, _d, _i64, _i64, _i, _i64, _p, _p, _p, _p, _p, _sz, _p]),
+    "sdb_cheb_reduce": (_i, [_p, _i64, _i64, _i, _p, _p, _p]),
     "sdb_moments_mean": (_i, [_p, _i64, _i64, _p, _p, _p]),
     "sdb_jackson_damping": (_i, [_i64, _p, _p]),
     "sdb_kpm_coefficients": (_i, [_p, _i64, _i64, _i, _p, _p]),

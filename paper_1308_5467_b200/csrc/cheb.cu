@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
     const int ix = r32 % nx, t = r32 / nx;
     const int iy = t % ny, iz = t / ny;
     const bool interior = (!S.mx || (ix > 0 && ix < nx - 1)) && (!S.my || (iy > 0 && iy < ny - 1)) &&
-                          (!S.mz || (iz > 0 && iz < nz - 1));
+                          (S.zghost || !S.mz || (iz > 0 && iz < nz - 1));
     const double dg = __ldg(S.diag + row);
     double2 y[VPL];
 #pragma unroll
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
             int jx = ix + tm.x, jy = iy + tm.y, jz = iz + tm.z;
             jx = jx < 0 ? jx + nx : (jx >= nx ? jx - nx : jx);
             jy = jy < 0 ? jy + ny : (jy >= ny ? jy - ny : jy);
-            jz = jz < 0 ? jz + nz : (jz >= nz ? jz - nz : jz);
+            if (!S.zghost) jz = jz < 0 ? jz + nz : (jz >= nz ? jz - nz : jz);
             col[u] = (jz * ny + jy) * nx + jx;
           }
         }
@@ -343,7 +343,8 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
       // wrapped offsets for d = -1, +1 along each axis
       const int xm = ix == 0 ? nx - 1 : -1, xp = ix == nx - 1 ? 1 - nx : 1;
       const int ym = iy == 0 ? (ny - 1) * nx : -nx, yp = iy == ny - 1 ? (1 - ny) * nx : nx;
-      const int zm = iz == 0 ? (nz - 1) * nxy : -nxy, zp = iz == nz - 1 ? (1 - nz) * nxy : nxy;
+      const int zm = (iz == 0 && !S.zghost) ? (nz - 1) * nxy : -nxy;
+      const int zp = (iz == nz - 1 && !S.zghost) ? (1 - nz) * nxy : nxy;
       double2 y[VPL];
 #pragma unroll
       for (int v = 0; v < VPL; ++v) y[v] = make_double2(0.0, 0.0);
@@ -586,6 +587,7 @@ static TilePlan plan_tile(const sdb_matrix* m, int64_t ldv, int mode) {
     if (p.smem > 227 * 1024) return p;  // does not fit: grid kernel instead
   }
   p.t.diag = m->diag;
+  p.t.zghost = m->zghost;
   // weights in lexicographic (dz, dy, dx) order = sorted term order
   for (int o = 0; o < 27; ++o) p.t.wc[o] = 0.0;
   const GridShapeTable tab = grid_shape_table(m->shape);
@@ -638,6 +640,95 @@ static void cheb_layout(const sdb_matrix* m, int64_t ldv, int64_t degree, size_t
   *partial_bytes = align256(sizeof(double) * (size_t)(degree + 1) * (size_t)bmax * (size_t)ldv);
 }
 
+// ---- step planning shared by the moment driver and the step-level ABI ------------
+struct StepPlan {
+  Geometry g;   // block geometry (ldv)
+  Geometry gk;  // geometry of the launched kernel (per column slice)
+  TilePlan tp;
+  StepArgs a;   // n, ldv, nblocks, panel, slices, c, inv_d filled
+  StencilView st;
+};
+
+static int plan_steps(const sdb_matrix* m, int64_t n_vec, int mode, double c, double d, StepPlan* P) {
+  SDB_REQUIRE(n_vec >= 1 && n_vec <= SDB_MAX_BATCH, "n_vec must lie in [1, %d] per batch", SDB_MAX_BATCH);
+  SDB_REQUIRE(mode == SDB_CHEB_DIRECT || mode == SDB_CHEB_DOUBLING, "unknown moment mode %d", mode);
+  StepPlan& p = *P;
+  p.g = choose_geometry(n_vec);
+  p.gk = p.g;
+  p.a = StepArgs{};
+  p.a.c = c;
+  p.a.inv_d = 1.0 / d;
+  p.a.n = m->n;
+  p.a.ldv = p.g.ldv;
+  p.tp = plan_tile(m, p.g.ldv, mode);
+  p.a.slices = 1;
+  if (!p.tp.on && m->format == SDB_FMT_STENCIL && (m->shape == SDB_SHAPE_FACE7 || m->shape == SDB_SHAPE_BOX27)) {
+    const int sl = env_int("SDB_GRID_SLICES", 1);
+    if (sl > 1 && p.g.ldv % (2 * sl) == 0) {
+      Geometry gs = choose_geometry(p.g.ldv / sl);
+      if (gs.ldv == p.g.ldv / sl) {
+        p.a.slices = sl;
+        p.gk = gs;
+      }
+    }
+  }
+  const int rpbk = (32 / p.gk.L) * kStepWarps;
+  p.a.nblocks = p.tp.on ? p.tp.nblocks : step_blocks(m, p.gk, rpbk) / p.a.slices;
+  if (p.a.nblocks < 1) p.a.nblocks = 1;
+  p.a.panel = panel_rows(m, p.g.ldv, rpbk);
+  p.st = StencilView{};
+  if (m->format == SDB_FMT_STENCIL) p.st = make_stencil_view(m);
+  return SDB_OK;
+}
+
+static int launch_plan_step(const sdb_matrix* m, const StepPlan& P, int64_t degree, int mode, int64_t k,
+                            const double* x, const double* prev, double* next, const double* v0, double* partials,
+                            cudaStream_t s) {
+  StepArgs a = P.a;
+  a.partials = partials;
+  a.v0 = v0;
+  int rc;
+  const int64_t steps = (mode == SDB_CHEB_DOUBLING) ? (degree + 1) / 2 : degree;
+  if (steps == 0) {  // degree 0: only zeta_0 = <v0, v0>
+    a.v0 = x;
+    a.slot0 = 0;
+    if ((rc = launch_self_dot(P.g, a, s))) return rc;
+    SDB_CHECK_LAUNCH();
+    return SDB_OK;
+  }
+  a.x = x;
+  a.prev = prev;
+  a.next = next;
+  a.slot0 = (k == 0) ? 0 : -1;
+  if (mode == SDB_CHEB_DOUBLING) {
+    a.slotB = (2 * k + 1 <= degree) ? (int)(2 * k + 1) : -1;
+    a.slotA = (2 * k + 2 <= degree) ? (int)(2 * k + 2) : -1;
+    if (P.tp.on)
+      rc = k == 0 ? launch_tile<true>(m, P.tp, a, s) : launch_tile<false>(m, P.tp, a, s);
+    else
+      rc = k == 0 ? launch_step<SDB_CHEB_DOUBLING, true>(m, P.gk, &P.st, a, s)
+                  : launch_step<SDB_CHEB_DOUBLING, false>(m, P.gk, &P.st, a, s);
+  } else {
+    a.slotA = (int)(k + 1);
+    a.slotB = -1;
+    rc = k == 0 ? launch_step<SDB_CHEB_DIRECT, true>(m, P.gk, &P.st, a, s)
+                : launch_step<SDB_CHEB_DIRECT, false>(m, P.gk, &P.st, a, s);
+  }
+  if (rc) return rc;
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+static int launch_reduce(const StepPlan& P, int64_t n_vec, int64_t degree, int mode, const double* partials,
+                         double* zeta_pp, cudaStream_t s) {
+  const int64_t total = n_vec * (degree + 1);
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 4096) blocks = 4096;
+  cheb_reduce_kernel<<<blocks, 256, 0, s>>>(partials, P.a.nblocks, P.g.ldv, n_vec, degree, mode, zeta_pp);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
 }  // namespace sdb
 
 using namespace sdb;
@@ -669,40 +760,13 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
   DeviceGuard dg(m->device);
   if (!dg.ok) return fail(SDB_ECUDA, "cannot select CUDA device %d", m->device);
   cudaStream_t s = (cudaStream_t)stream;
-  Geometry g = choose_geometry(n_vec);
+  StepPlan P;
+  if ((rc = plan_steps(m, n_vec, mode, c, d, &P))) return rc;
   size_t bb, pb;
-  cheb_layout(m, g.ldv, degree, &bb, &pb);
+  cheb_layout(m, P.g.ldv, degree, &bb, &pb);
   double* bufA = (double*)workspace;
   double* bufB = (double*)((char*)workspace + bb);
   double* partials = (double*)((char*)workspace + 2 * bb);
-
-  StepArgs a{};
-  a.v0 = probes;
-  a.c = c;
-  a.inv_d = 1.0 / d;
-  a.n = m->n;
-  a.ldv = g.ldv;
-  const int rpb = (32 / g.L) * kStepWarps;
-  const TilePlan tp = plan_tile(m, g.ldv, mode);
-  a.slices = 1;
-  Geometry gk = g;  // geometry of the launched step kernel (per column slice)
-  if (!tp.on && m->format == SDB_FMT_STENCIL && (m->shape == SDB_SHAPE_FACE7 || m->shape == SDB_SHAPE_BOX27)) {
-    const int sl = env_int("SDB_GRID_SLICES", 1);
-    if (sl > 1 && g.ldv % (2 * sl) == 0) {
-      Geometry gs = choose_geometry(g.ldv / sl);
-      if (gs.ldv == g.ldv / sl) {
-        a.slices = sl;
-        gk = gs;
-      }
-    }
-  }
-  const int rpbk = (32 / gk.L) * kStepWarps;
-  a.nblocks = tp.on ? tp.nblocks : step_blocks(m, gk, rpbk) / a.slices;
-  if (a.nblocks < 1) a.nblocks = 1;
-  a.panel = panel_rows(m, g.ldv, rpbk);
-  a.partials = partials;
-  StencilView st{};
-  if (m->format == SDB_FMT_STENCIL) st = make_stencil_view(m);
 
   const int64_t steps = (mode == SDB_CHEB_DOUBLING) ? (degree + 1) / 2 : degree;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -711,47 +775,16 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
     SDB_CUDA(cudaEventCreate(&e1));
     SDB_CUDA(cudaEventRecord(e0, s));
   }
-  if (steps == 0) {
-    a.slot0 = 0;
-    rc = launch_self_dot(g, a, s);
-    if (rc) return rc;
-    SDB_CHECK_LAUNCH();
-  }
   const double* cur = probes;
   const double* prev = nullptr;
-  for (int64_t k = 0; k < steps; ++k) {
+  for (int64_t k = 0; k < (steps > 0 ? steps : 1); ++k) {
     double* next = (k == 0) ? bufA : (k == 1 ? bufB : const_cast<double*>(prev));
-    a.x = cur;
-    a.prev = prev;
-    a.next = next;
-    a.slot0 = (k == 0) ? 0 : -1;
-    if (mode == SDB_CHEB_DOUBLING) {
-      a.slotB = (2 * k + 1 <= degree) ? (int)(2 * k + 1) : -1;
-      a.slotA = (2 * k + 2 <= degree) ? (int)(2 * k + 2) : -1;
-      if (tp.on)
-        rc = k == 0 ? launch_tile<true>(m, tp, a, s) : launch_tile<false>(m, tp, a, s);
-      else
-        rc = k == 0 ? launch_step<SDB_CHEB_DOUBLING, true>(m, gk, &st, a, s)
-                    : launch_step<SDB_CHEB_DOUBLING, false>(m, gk, &st, a, s);
-    } else {
-      a.slotA = (int)(k + 1);
-      a.slotB = -1;
-      rc = k == 0 ? launch_step<SDB_CHEB_DIRECT, true>(m, gk, &st, a, s)
-                  : launch_step<SDB_CHEB_DIRECT, false>(m, gk, &st, a, s);
-    }
-    if (rc) return rc;
-    SDB_CHECK_LAUNCH();
+    if ((rc = launch_plan_step(m, P, degree, mode, k, cur, prev, next, probes, partials, s))) return rc;
     prev = cur;
     cur = next;
   }
   if (step_ms) SDB_CUDA(cudaEventRecord(e1, s));
-  {
-    int64_t total = n_vec * (degree + 1);
-    int blocks = (int)((total + 255) / 256);
-    if (blocks > 4096) blocks = 4096;
-    cheb_reduce_kernel<<<blocks, 256, 0, s>>>(partials, a.nblocks, g.ldv, n_vec, degree, mode, zeta_pp);
-    SDB_CHECK_LAUNCH();
-  }
+  if ((rc = launch_reduce(P, n_vec, degree, mode, partials, zeta_pp, s))) return rc;
   if (step_ms) {
     SDB_CUDA(cudaEventSynchronize(e1));
     SDB_CUDA(cudaEventElapsedTime(step_ms, e0, e1));
@@ -759,6 +792,51 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
     cudaEventDestroy(e1);
   }
   return SDB_OK;
+}
+
+int sdb_cheb_partials_size(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode, size_t* bytes) {
+  SDB_REQUIRE(m && bytes, "NULL argument");
+  size_t need = 0;
+  int rc = sdb_cheb_workspace_size(m, n_vec, degree, mode, &need);
+  if (rc) return rc;
+  size_t bb, pb;
+  cheb_layout(m, choose_geometry(n_vec).ldv, degree, &bb, &pb);
+  *bytes = pb;
+  return SDB_OK;
+}
+
+int sdb_cheb_step(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode, int64_t k,
+                  const double* x, const double* prev, double* next, const double* v0, double* partials,
+                  size_t partial_bytes, void* stream) {
+  SDB_REQUIRE(m && x && partials, "NULL argument");
+  size_t pb = 0;
+  int rc = sdb_cheb_partials_size(m, n_vec, degree, mode, &pb);
+  if (rc) return rc;
+  SDB_REQUIRE(partial_bytes >= pb, "partials buffer too small (%zu < %zu bytes)", partial_bytes, pb);
+  const int64_t steps = (mode == SDB_CHEB_DOUBLING) ? (degree + 1) / 2 : degree;
+  SDB_REQUIRE(k >= 0 && (k < steps || (steps == 0 && k == 0)), "step %lld outside [0, %lld)", (long long)k,
+              (long long)steps);
+  SDB_REQUIRE(steps == 0 || next != nullptr, "next must not be NULL");
+  SDB_REQUIRE(k == 0 || prev != nullptr, "prev must not be NULL after the first step");
+  SDB_REQUIRE(mode != SDB_CHEB_DIRECT || v0 != nullptr || k == 0, "direct mode needs v0");
+  SDB_REQUIRE(d != 0.0, "spectral halfwidth must be non-zero");
+  DeviceGuard dg(m->device);
+  if (!dg.ok) return fail(SDB_ECUDA, "cannot select CUDA device %d", m->device);
+  StepPlan P;
+  if ((rc = plan_steps(m, n_vec, mode, c, d, &P))) return rc;
+  return launch_plan_step(m, P, degree, mode, k, x, prev, next, v0 ? v0 : x, partials, (cudaStream_t)stream);
+}
+
+int sdb_cheb_reduce(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode, const double* partials,
+                    double* zeta_pp, void* stream) {
+  SDB_REQUIRE(m && partials && zeta_pp, "NULL argument");
+  SDB_REQUIRE(n_vec >= 1 && n_vec <= SDB_MAX_BATCH && degree >= 0, "bad shape");
+  DeviceGuard dg(m->device);
+  if (!dg.ok) return fail(SDB_ECUDA, "cannot select CUDA device %d", m->device);
+  StepPlan P;
+  int rc = plan_steps(m, n_vec, mode, 0.0, 1.0, &P);
+  if (rc) return rc;
+  return launch_reduce(P, n_vec, degree, mode, partials, zeta_pp, (cudaStream_t)stream);
 }
 
 int sdb_moments_mean(const double* zeta_pp, int64_t n_vec, int64_t degree, double* zeta, int32_t* nonfinite,

@@ -75,6 +75,7 @@ struct sdb_matrix {
   double term_w_host[27] = {};
   int nterms = 0, center_pos = 0, mx = 0, my = 0, mz = 0;
   int shape = 0;              // SDB_SHAPE_*: specialised grid kernel available
+  int zghost = 0;             // z-slab of a row partition (no z wrap, ghost planes)
 };
 
 namespace sdb {

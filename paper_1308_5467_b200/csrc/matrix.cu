@@ -305,11 +305,12 @@ int sdb_matrix_create_stencil(int device, const sdb_stencil_desc* desc, const do
     }
   }
   m->nterms = nt;
+  m->zghost = desc->z_ghost ? 1 : 0;
   for (int o = 0; o < nt; ++o) m->term_w_host[o] = tw[o];
   // shape detection: 6 face neighbours or the full 3x3x3 box, with every
   // extent >= 3 so the lexicographic term order is the sorted one
   {
-    bool dims_ok = desc->nx >= 3 && desc->ny >= 3 && desc->nz >= 3;
+    bool dims_ok = desc->nx >= 3 && desc->ny >= 3 && (desc->nz >= 3 || desc->z_ghost);
     auto has = [&](int dx, int dy, int dz) {
       for (int o = 0; o < desc->n_offsets; ++o)
         if (desc->offsets[o][0] == dx && desc->offsets[o][1] == dy && desc->offsets[o][2] == dz) return true;

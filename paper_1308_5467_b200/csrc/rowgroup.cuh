@@ -200,6 +200,7 @@ struct StencilView {
   int nterms;          // off-centre points + 1
   int center_pos;      // index of the diagonal term
   int mx, my, mz;      // does any offset move along x / y / z
+  int zghost;          // z-slab: no z wrap (ghost planes next to the slab)
   const int4* term;    // (dx, dy, dz, interior column delta), device, nterms
   const double* tw;    // term weights (the diagonal's comes from diag[])
   const double* diag;
@@ -222,7 +223,7 @@ __device__ __forceinline__ void spmv_row(const StencilView& S, int64_t row, bool
     int jx = ix + tm.x, jy = iy + tm.y, jz = iz + tm.z;
     jx = jx < 0 ? jx + S.nx : (jx >= S.nx ? jx - S.nx : jx);
     jy = jy < 0 ? jy + S.ny : (jy >= S.ny ? jy - S.ny : jy);
-    jz = jz < 0 ? jz + S.nz : (jz >= S.nz ? jz - S.nz : jz);
+    if (!S.zghost) jz = jz < 0 ? jz + S.nz : (jz >= S.nz ? jz - S.nz : jz);
     const int64_t col = ((int64_t)jz * S.ny + jy) * S.nx + jx;
     const double wt = (o == S.center_pos) ? dg : __ldg(S.tw + o);
     const double* xr = x + col * ldv + 2 * q;
@@ -245,6 +246,7 @@ inline StencilView make_stencil_view(const sdb_matrix* m) {
   s.mx = m->mx;
   s.my = m->my;
   s.mz = m->mz;
+  s.zghost = m->zghost;
   s.term = m->terms;
   s.tw = m->term_w;
   s.diag = m->diag;

@@ -24,6 +24,7 @@ struct TileArgs {
   int n_xt, n_yt, n_zs;  // tiles in x, y and z segments
   int ZS;                // planes per z segment
   int slices;            // column slices (ldv / CS)
+  int zghost;            // z-slab: no z wrap (ghost planes next to the slab)
   const double* diag;
   double wc[27];         // weights in lexicographic (dz,dy,dx) order; centre unused
 };
@@ -131,8 +132,9 @@ __global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, St
   const double2* pg = reinterpret_cast<const double2*>(a.prev + col0);
   const int64_t plane_units = plane_rows * (a.ldv / 2);  // 16-byte units per plane
   auto load_plane = [&](int z) {
-    z = z < 0 ? z + nz : (z >= nz ? z - nz : z);
-    double* dst = planes + (size_t)(((z % SM::R) + SM::R) % SM::R) * SM::PLANE;
+    const int zs_ = z;  // ring slot follows the unwrapped plane index
+    if (!t.zghost) z = z < 0 ? z + nz : (z >= nz ? z - nz : z);
+    double* dst = planes + (size_t)(((zs_ % SM::R) + SM::R) % SM::R) * SM::PLANE;
     const double2* src = xg + (int64_t)z * plane_units;
 #pragma unroll
     for (int k = 0; k < NCH; ++k)

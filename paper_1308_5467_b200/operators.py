@@ -91,6 +91,8 @@ class StencilOperator:
     on exactly the same operator.
     """
 
+    z_ghost = False  # see SlabStencil
+
     def __init__(self, shape, offsets, weights, diag):
         self.shape = tuple(int(s) for s in shape)
         if len(self.shape) != 3 or min(self.shape) < 1:
@@ -153,6 +155,36 @@ class StencilOperator:
 
     def matvec(self, x):  # interop only; the engine never calls it
         return self.csr @ x
+
+
+class SlabStencil(StencilOperator):
+    """Planes [z0, z1) of a periodic StencilOperator, for the row partition.
+
+    The slab's operator is not periodic in z: the neighbours of its first and
+    last plane live in ghost planes that the caller keeps immediately before
+    and after the slab's rows in every block (sdb_stencil_desc.z_ghost).
+    """
+
+    z_ghost = True
+
+    def __init__(self, parent, z0, z1):
+        nx, ny, nz = parent.shape
+        if not (0 <= z0 < z1 <= nz):
+            raise ValueError(f"bad slab [{z0}, {z1}) of {nz} planes")
+        self.parent = parent
+        self.z0, self.z1 = int(z0), int(z1)
+        self.shape = (nx, ny, self.z1 - self.z0)
+        self.offsets = list(parent.offsets)
+        self.weights = list(parent.weights)
+        self.diag = np.ascontiguousarray(parent.diag[self.z0 * nx * ny:self.z1 * nx * ny])
+        self._csr = None
+
+    @property
+    def csr(self):
+        raise TypeError("a slab has no standalone CSR form (its z neighbours live on other ranks)")
+
+    def matvec(self, x):
+        raise TypeError("a slab has no standalone matvec")
 
 
 class MappedOperator:
@@ -394,6 +426,7 @@ class DeviceMatrix:
             desc = _native.SdbStencilDesc()
             desc.nx, desc.ny, desc.nz = base.shape
             desc.n_offsets = len(base.offsets)
+            desc.z_ghost = 1 if getattr(base, "z_ghost", False) else 0
             for i, (o, w) in enumerate(zip(base.offsets, base.weights)):
                 for a in range(3):
                     desc.offsets[i][a] = o[a]

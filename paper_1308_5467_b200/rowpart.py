@@ -1,0 +1,204 @@
+"""Row-partitioned KPM moments for periodic stencils.
+
+The grid's z-planes are split into contiguous slabs, one per rank (GPU).
+Each slab keeps, in every n x ldv block it holds, one ghost plane below and
+one above its own planes.  Per recurrence step:
+
+  1. every slab runs the fused step kernel on its own rows (``sdb_cheb_step``
+     with a z-ghost stencil handle: z is not wrapped, the neighbours of the
+     first / last own plane are read from the ghost planes);
+  2. halo exchange: a slab's first own plane of w_{k+1} becomes the upper
+     ghost of the slab below it, its last own plane the lower ghost of the
+     slab above it (periodic in z) -- a device copy when both slabs live in
+     this process, an NCCL send/recv pair otherwise (2 x nx*ny*ldv*8 bytes
+     received per slab per step: 33.6 MB at 256^3 with 32 probes).
+
+Moments are sums over rows, so each slab reduces its own partials into
+per-probe moments and one all-reduce over ranks at the end gives the global
+per-probe moments (the doubling transform is linear, so it commutes with the
+sum).  The step's compute and the driver's exchange are passed in as
+callables so the same driver runs the CUDA path (``DeviceSlab``) and a CPU
+reference slab in the multi-process gloo tests.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from . import engine as E
+from .distributed import shard_range
+from .operators import SlabStencil, StencilOperator, device_matrix
+
+
+@dataclass
+class SlabPlan:
+    """Which planes each slab owns."""
+
+    nz: int
+    n_slabs: int
+
+    def planes(self, s):
+        return shard_range(self.nz, self.n_slabs, s)  # (z0, count)
+
+    def neighbours(self, s):
+        return (s - 1) % self.n_slabs, (s + 1) % self.n_slabs
+
+
+def halo_exchange(slabs, plan, blocks, group=None, rank_of_slab=None):
+    """Refresh the ghost planes of ``blocks[s]`` for every local slab s.
+
+    ``slabs``: local slab indices; ``blocks[s]``: tensor view (nzl+2, nxy, ldv)
+    of slab s's current w block (ghost planes at [0] and [-1]).
+    ``rank_of_slab``: maps a slab to its rank (None -> all slabs local).
+    """
+    import torch.distributed as dist
+
+    local = set(slabs)
+    ops = []
+    for s in slabs:
+        lo, hi = plan.neighbours(s)
+        blk = blocks[s]
+        # ghost below = last own plane of slab lo; ghost above = first own plane of slab hi
+        if lo in local:
+            blk[0].copy_(blocks[lo][-2])
+        if hi in local:
+            blk[-1].copy_(blocks[hi][1])
+    if rank_of_slab is None:
+        return
+    for s in slabs:  # sends first, then receives (matching order for any world size)
+        lo, hi = plan.neighbours(s)
+        blk = blocks[s]
+        if lo not in local:
+            ops.append(dist.P2POp(dist.isend, blk[1].contiguous() if not blk[1].is_contiguous() else blk[1],
+                                  rank_of_slab(lo), group))
+        if hi not in local:
+            ops.append(dist.P2POp(dist.isend, blk[-2], rank_of_slab(hi), group))
+    for s in slabs:
+        lo, hi = plan.neighbours(s)
+        blk = blocks[s]
+        if hi not in local:
+            ops.append(dist.P2POp(dist.irecv, blk[-1], rank_of_slab(hi), group))
+        if lo not in local:
+            ops.append(dist.P2POp(dist.irecv, blk[0], rank_of_slab(lo), group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
+def ghosted_probe_block(source, start, count, parent_shape, z0, nzl, ldv, out):
+    """Fill ``out`` (nzl+2, nxy, ldv) with planes z0-1 .. z0+nzl (periodic) of
+    probes start..start+count-1, padding columns zero."""
+    nx, ny, nz = parent_shape
+    nxy = nx * ny
+    planes = [(z0 - 1) % nz] + list(range(z0, z0 + nzl)) + [(z0 + nzl) % nz]
+    host = np.zeros((nzl + 2, nxy, ldv))
+    for l in range(count):
+        v = np.asarray(source.draw(start + l)).reshape(nz, nxy)
+        host[:, :, l] = v[planes]
+    out.copy_(__import__("torch").from_numpy(host))
+
+
+class DeviceSlab:
+    """One slab on one GPU: z-ghost stencil handle + ghosted blocks."""
+
+    def __init__(self, op, plan, s, n_vec, degree, mode, device):
+        import torch
+
+        self.s = s
+        self.z0, self.nzl = plan.planes(s)
+        self.slab = SlabStencil(op, self.z0, self.z0 + self.nzl)
+        self.device = device
+        self.stream = E.stream_ptr(device)
+        self.dm = device_matrix(self.slab, device, self.stream)
+        self.ldv = E.block_ldv(n_vec)
+        nx, ny, _ = op.shape
+        self.nxy = nx * ny
+        shape = (self.nzl + 2, self.nxy, self.ldv)
+        self.blocks = [torch.zeros(shape, dtype=torch.float64, device=device) for _ in range(3)]
+        need = __import__("ctypes").c_size_t()
+        _native.check(_native.load().sdb_cheb_partials_size(self.dm.handle, n_vec, degree, mode,
+                                                            __import__("ctypes").byref(need)))
+        self.partials = torch.empty(max(need.value, 8) // 8 + 1, dtype=torch.float64, device=device)
+        self.n_vec, self.degree, self.mode = n_vec, degree, mode
+
+    def own(self, t):
+        """Pointer to the first own row of a ghosted block."""
+        return E.ptr(t[1])
+
+    def step(self, k, c, d, cur, prev, nxt, v0):
+        _native.call("sdb_cheb_step", self.dm.handle, c, d, self.n_vec, self.degree, self.mode, k, self.own(cur),
+                     self.own(prev) if prev is not None else None, self.own(nxt), self.own(v0),
+                     E.ptr(self.partials), self.partials.numel() * 8, self.stream)
+
+    def reduce(self):
+        import torch
+
+        zeta_pp = torch.empty((self.n_vec, self.degree + 1), dtype=torch.float64, device=self.device)
+        _native.call("sdb_cheb_reduce", self.dm.handle, self.n_vec, self.degree, self.mode, E.ptr(self.partials),
+                     E.ptr(zeta_pp), self.stream)
+        return zeta_pp
+
+
+def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=None):
+    """Drive the recurrence over local slab objects (DeviceSlab or a CPU
+    stand-in with the same interface: .blocks (3 ghosted blocks, block 0 holds
+    the probes), .step(k, c, d, cur, prev, next, v0), .reduce()).
+
+    Returns the per-probe moments of the whole grid (sum over all slabs,
+    all-reduced over ``group`` when slabs live on several ranks)."""
+    import torch.distributed as dist
+
+    steps = (degree + 1) // 2 if mode == _native.SDB_CHEB_DOUBLING else degree
+    ids = [sl.s for sl in slabs]
+    cur = {sl.s: sl.blocks[0] for sl in slabs}
+    prev = {sl.s: None for sl in slabs}
+    for k in range(max(steps, 1)):
+        nxt = {}
+        for sl in slabs:
+            nxt[sl.s] = sl.blocks[1] if k == 0 else (sl.blocks[2] if k == 1 else prev[sl.s])
+            sl.step(k, c, d, cur[sl.s], prev[sl.s], nxt[sl.s], sl.blocks[0])
+        if steps > 0 and k + 1 < steps:
+            halo_exchange(ids, plan, nxt, group, rank_of_slab)
+        prev, cur = cur, nxt
+    total = None
+    for sl in slabs:
+        z = sl.reduce()
+        total = z if total is None else total + z
+    if rank_of_slab is not None:
+        dist.all_reduce(total, op=dist.ReduceOp.SUM, group=group)
+    return total
+
+
+def rowpartition_moments(op, interval, degree, source, n_vec, mode=_native.SDB_CHEB_DOUBLING, n_slabs=None,
+                         group=None, device=None):
+    """Per-probe moments of (A - cI)/d for a periodic StencilOperator with the
+    z-planes row-partitioned: one slab per rank of ``group`` (or ``n_slabs``
+    slabs in this process when no group is given -- the single-GPU form used
+    by the tests).  Returns a (n_vec, degree+1) device tensor."""
+    import torch
+    import torch.distributed as dist
+
+    if not isinstance(op, StencilOperator) or getattr(op, "z_ghost", False):
+        raise TypeError("row partition needs a periodic StencilOperator")
+    if not 1 <= n_vec <= _native.SDB_MAX_BATCH:
+        raise ValueError("row-partitioned moments take one probe batch (n_vec <= 256)")
+    device = E.require_cuda(device)
+    c, d = float(interval.center), float(interval.halfwidth)
+    nz = op.shape[2]
+    if group is not None or (dist.is_available() and dist.is_initialized() and n_slabs is None):
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        plan = SlabPlan(nz, world)
+        local = [rank]
+        rank_of_slab = lambda s: s  # noqa: E731
+    else:
+        plan = SlabPlan(nz, n_slabs or 1)
+        local = list(range(plan.n_slabs))
+        rank_of_slab = None
+    if min(plan.planes(s)[1] for s in range(plan.n_slabs)) < 1:
+        raise ValueError("more slabs than z-planes")
+    with torch.cuda.device(device):
+        slabs = [DeviceSlab(op, plan, s, n_vec, degree, mode, device) for s in local]
+        for sl in slabs:
+            ghosted_probe_block(source, 0, n_vec, op.shape, sl.z0, sl.nzl, sl.ldv, sl.blocks[0])
+        return run_rowpartition(slabs, plan, c, d, degree, mode, group if rank_of_slab else None, rank_of_slab)

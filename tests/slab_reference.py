@@ -1,0 +1,66 @@
+"""CPU stand-in for rowpart.DeviceSlab (test infrastructure only): the same
+interface, with the step restated in NumPy on the ghosted slab blocks."""
+
+import numpy as np
+import torch
+
+from paper_1308_5467_b200.distributed import shard_range
+
+
+class NumpySlab:
+    def __init__(self, op, plan, s, n_vec, degree, doubling=True):
+        self.s = s
+        self.z0, self.nzl = plan.planes(s)
+        nx, ny, nz = op.shape
+        self.nx, self.ny, self.nxy = nx, ny, nx * ny
+        self.offsets, self.weights = op.offsets, op.weights
+        self.diag = op.diag.reshape(nz, ny, nx)[self.z0:self.z0 + self.nzl]
+        self.n_vec, self.degree, self.doubling = n_vec, degree, doubling
+        shape = (self.nzl + 2, self.nxy, n_vec)
+        self.blocks = [torch.zeros(shape, dtype=torch.float64) for _ in range(3)]
+        self.raw = np.zeros((degree + 1, n_vec))
+
+    def _own(self, t):
+        return t[1:-1].numpy().reshape(self.nzl, self.ny, self.nx, self.n_vec)
+
+    def step(self, k, c, d, cur, prev, nxt, v0):
+        g = cur.numpy().reshape(self.nzl + 2, self.ny, self.nx, self.n_vec)
+        x = g[1:-1]
+        y = self.diag[..., None] * x
+        for (dx, dy, dz), w in zip(self.offsets, self.weights):
+            nb = g[1 + dz:1 + dz + self.nzl]
+            nb = np.roll(np.roll(nb, -dy, axis=1), -dx, axis=2)
+            y = y + w * nb
+        t = (y - c * x) / d
+        if k == 0:
+            wn = t
+        else:
+            wn = 2.0 * t - self._own(prev)
+        nxt[1:-1] = torch.from_numpy(wn.reshape(self.nzl, self.nxy, self.n_vec))
+        red = lambda a, b: np.einsum("zyxl,zyxl->l", a, b)  # noqa: E731
+        if self.doubling:
+            if k == 0:
+                self.raw[0] += red(x, x)
+            if 2 * k + 1 <= self.degree:
+                self.raw[2 * k + 1] += red(wn, x)
+            if 2 * k + 2 <= self.degree:
+                self.raw[2 * k + 2] += red(wn, wn)
+        else:
+            p = self._own(v0)
+            if k == 0:
+                self.raw[0] += red(p, p)
+            self.raw[k + 1] += red(p, wn)
+
+    def reduce(self):
+        z = self.raw.copy()
+        if self.doubling:
+            for k in range(2, self.degree + 1):
+                z[k] = 2.0 * self.raw[k] - self.raw[k % 2]
+        return torch.from_numpy(z.T.copy())
+
+
+def fill_probes(slab, probes, parent_shape):
+    nx, ny, nz = parent_shape
+    planes = [(slab.z0 - 1) % nz] + list(range(slab.z0, slab.z0 + slab.nzl)) + [(slab.z0 + slab.nzl) % nz]
+    v = probes.reshape(probes.shape[0], nz, nx * ny)[:, planes]  # (n_vec, nzl+2, nxy)
+    slab.blocks[0].copy_(torch.from_numpy(np.ascontiguousarray(v.transpose(1, 2, 0))))

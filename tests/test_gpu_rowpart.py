@@ -1,0 +1,43 @@
+"""Row-partitioned stencil moments on the GPU: z-ghost slab kernels, several
+slabs driven in one process (halo planes exchanged by device copies).  The
+multi-rank exchange itself is covered on CPU (tests/test_rowpart_cpu.py)."""
+
+import numpy as np
+import pytest
+
+import paper_1308_5467_b200 as sdb
+from oracle import specdens_oracle as O
+from paper_1308_5467_b200 import workloads as W
+from paper_1308_5467_b200.rowpart import rowpartition_moments
+
+pytestmark = pytest.mark.gpu
+
+
+def generic_stencil():
+    rng = np.random.default_rng(3)
+    offs = [(1, 0, 0), (-1, 0, 0), (1, 1, 1), (-1, -1, -1), (0, 0, 1), (0, 0, -1)]
+    return sdb.StencilOperator((6, 5, 8), offs, [0.3, 0.3, -0.2, -0.2, 0.5, 0.5], rng.uniform(-1, 1, 240))
+
+
+@pytest.mark.parametrize("builder", [lambda: W.anderson_3d(8), lambda: W.stencil27_3d(7), generic_stencil],
+                         ids=["face7", "box27", "generic"])
+@pytest.mark.parametrize("n_slabs", [1, 2, 3, 4])
+@pytest.mark.parametrize("mode", [1, 0], ids=["doubling", "direct"])
+def test_slabs_match_oracle(builder, n_slabs, mode):
+    op = builder()
+    iv = W.gershgorin_interval(op)
+    n_vec, deg = 20, 31
+    src = sdb.ProbeVectorSource("rademacher", seed=4, dim=op.dim)
+    got = rowpartition_moments(op, iv, deg, src, n_vec, mode=mode, n_slabs=n_slabs).cpu().numpy()
+    ref = O.chebyshev_moments(op.csr, iv.center, iv.halfwidth, deg, "rademacher", 4, n_vec, mode="direct")
+    assert np.max(np.abs(got - ref)) <= 1e-10 * np.max(np.abs(ref))
+
+
+def test_slabs_match_unpartitioned_large():
+    op = W.stencil27_3d(32)
+    iv = W.gershgorin_interval(op)
+    src = sdb.ProbeVectorSource("rademacher", seed=0, dim=op.dim)
+    whole = sdb.moments_via_product_formula(sdb.apply_spectral_map(op, iv), 60, src, 32)
+    for n_slabs in (2, 8):
+        got = rowpartition_moments(op, iv, 60, src, 32, n_slabs=n_slabs).mean(dim=0).cpu().numpy()
+        assert np.max(np.abs(got - whole.zeta)) <= 1e-12 * np.max(np.abs(whole.zeta))
