@@ -31,10 +31,13 @@ constexpr int kStepWarps = kRowWarps;
 #define SDB_MINB_V1 5
 #endif
 #ifndef SDB_MINB_V2
-#define SDB_MINB_V2 4
+#define SDB_MINB_V2 2
 #endif
 #ifndef SDB_U_V1
 #define SDB_U_V1 4
+#endif
+#ifndef SDB_U_V2
+#define SDB_U_V2 8
 #endif
 __host__ __device__ constexpr int step_min_blocks(int l, int vpl) {
   return l < 8 ? (vpl == 1 ? 4 : 2) : (vpl == 1 ? SDB_MINB_V1 : (vpl == 2 ? SDB_MINB_V2 : 2));
@@ -163,7 +166,7 @@ template <int L, int VPL, int MODE, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_step_csr(CsrView A, StepArgs a) {
   constexpr int RPW = 32 / L;
   constexpr int RPB = RPW * kStepWarps;
-  constexpr int U = L < 4 ? L : (VPL == 1 ? SDB_U_V1 : 2);
+  constexpr int U = L < 4 ? L : (VPL == 1 ? SDB_U_V1 : (VPL == 2 ? SDB_U_V2 : 2));
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane / L, q = lane % L;
   const uint64_t pol = policy_evict_first();

@@ -58,6 +58,10 @@ def block_ldv(n_vec):
 
 def batches(n_vec, batch=_native.SDB_MAX_BATCH):
     """Contiguous probe ranges of at most ``batch`` probes."""
+    import os
+
+    if os.environ.get("SDB_BATCH"):
+        batch = max(1, min(batch, int(os.environ["SDB_BATCH"])))
     return [(s, min(batch, n_vec - s)) for s in range(0, n_vec, batch)]
 
 
