@@ -486,6 +486,12 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
     const double* vprev = j > 0 ? basis + (size_t)(j - 1) * plane : nullptr;
     if (m->format == SDB_FMT_CSR)
       rc = lz_launch_spmm(cv, g, wraw, vprev, vj, W1, st, j == 0, c, 1.0 / d, n, nrb, panel, part, s);
+    else if (m->shape == SDB_SHAPE_FACE7)
+      rc = lz_launch_spmm(make_grid_view<SDB_SHAPE_FACE7>(m), g, wraw, vprev, vj, W1, st, j == 0, c, 1.0 / d, n, nrb,
+                          panel, part, s);
+    else if (m->shape == SDB_SHAPE_BOX27)
+      rc = lz_launch_spmm(make_grid_view<SDB_SHAPE_BOX27>(m), g, wraw, vprev, vj, W1, st, j == 0, c, 1.0 / d, n, nrb,
+                          panel, part, s);
     else
       rc = lz_launch_spmm(sv, g, wraw, vprev, vj, W1, st, j == 0, c, 1.0 / d, n, nrb, panel, part, s);
     if (rc) return rc;

@@ -236,6 +236,90 @@ __device__ __forceinline__ void spmv_row(const StencilView& S, int64_t row, bool
   }
 }
 
+// 7-point-face / 27-point-box grids with compile-time term order
+// (lexicographic in (dz, dy, dx) = sorted-column order) and weights in the
+// kernel-parameter constant bank.
+template <int SHAPE>
+struct GridView {
+  int nx, ny, nz, zghost;
+  const double* diag;
+  double wc[27];
+};
+
+template <int SHAPE>
+struct GridTerms;
+template <>
+struct GridTerms<SDB_SHAPE_FACE7> {
+  static constexpr int NT = 7;
+  __host__ __device__ static constexpr int dx(int o) { return o == 2 ? -1 : (o == 4 ? 1 : 0); }
+  __host__ __device__ static constexpr int dy(int o) { return o == 1 ? -1 : (o == 5 ? 1 : 0); }
+  __host__ __device__ static constexpr int dz(int o) { return o == 0 ? -1 : (o == 6 ? 1 : 0); }
+};
+template <>
+struct GridTerms<SDB_SHAPE_BOX27> {
+  static constexpr int NT = 27;
+  __host__ __device__ static constexpr int dx(int o) { return o % 3 - 1; }
+  __host__ __device__ static constexpr int dy(int o) { return (o / 3) % 3 - 1; }
+  __host__ __device__ static constexpr int dz(int o) { return o / 9 - 1; }
+};
+
+template <int L, int VPL, int SHAPE>
+__device__ __forceinline__ void spmv_row(const GridView<SHAPE>& S, int64_t row, bool valid, int safe,
+                                         const double* __restrict__ x, int64_t ldv, int q, double2 (&y)[VPL]) {
+  using G = GridTerms<SHAPE>;
+#pragma unroll
+  for (int v = 0; v < VPL; ++v) y[v] = make_double2(0.0, 0.0);
+  if (!valid) return;
+  const int nx = S.nx, ny = S.ny, nz = S.nz, nxy = nx * ny;
+  const int r32 = (int)row;
+  const int ix = r32 % nx, t = r32 / nx;
+  const int iy = t % ny, iz = t / ny;
+  const int xm = ix == 0 ? nx - 1 : -1, xp = ix == nx - 1 ? 1 - nx : 1;
+  const int ym = iy == 0 ? (ny - 1) * nx : -nx, yp = iy == ny - 1 ? (1 - ny) * nx : nx;
+  const int zm = (iz == 0 && !S.zghost) ? (nz - 1) * nxy : -nxy;
+  const int zp = (iz == nz - 1 && !S.zghost) ? (1 - nz) * nxy : nxy;
+  const double dg = __ldg(S.diag + row);
+  constexpr int U = VPL == 1 ? 4 : 2;
+#pragma unroll
+  for (int o0 = 0; o0 < G::NT; o0 += U) {
+    double2 xv[U][VPL];
+    double w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int o = o0 + u;
+      int col = r32;
+      w[u] = 0.0;
+      if (o < G::NT) {
+        col = r32 + (G::dx(o) < 0 ? xm : (G::dx(o) > 0 ? xp : 0)) + (G::dy(o) < 0 ? ym : (G::dy(o) > 0 ? yp : 0)) +
+              (G::dz(o) < 0 ? zm : (G::dz(o) > 0 ? zp : 0));
+        w[u] = (G::dx(o) == 0 && G::dy(o) == 0 && G::dz(o) == 0) ? dg : S.wc[o];
+      }
+      const double* xr = x + (int64_t)col * ldv + 2 * q;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) xv[u][v] = ld_d2(xr + 2 * L * v);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        y[v].x = fma(w[u], xv[u][v].x, y[v].x);
+        y[v].y = fma(w[u], xv[u][v].y, y[v].y);
+      }
+  }
+}
+
+template <int SHAPE>
+inline GridView<SHAPE> make_grid_view(const sdb_matrix* m) {
+  GridView<SHAPE> g{};
+  g.nx = (int)m->st.nx;
+  g.ny = (int)m->st.ny;
+  g.nz = (int)m->st.nz;
+  g.zghost = m->zghost;
+  g.diag = m->diag;
+  for (int o = 0; o < 27; ++o) g.wc[o] = o < m->nterms ? m->term_w_host[o] : 0.0;
+  return g;
+}
+
 inline StencilView make_stencil_view(const sdb_matrix* m) {
   StencilView s{};
   s.nx = (int)m->st.nx;
