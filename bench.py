@@ -326,7 +326,8 @@ def main():
     internal = ("stencil (detected from CSR)" if dm.detected_stencil else
                 ("stencil" if dm.format == _native.SDB_FMT_STENCIL else "csr"))
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "kernel": "cheb_step_kernel", "peak_source": f"{peak_kind} hbm_gbs",
+            "traffic": traffic,
+            "kernel": "cheb_step_grid (7-point)" if dm.format == _native.SDB_FMT_STENCIL else "cheb_step_csr", "peak_source": f"{peak_kind} hbm_gbs",
             "bytes_per_launch": bytes_launch, "launches_per_step": launches,
             "avg_launch_us": avg_launch_s * 1e6, "kernel_share_of_step": k_ms / t_ms, "ldv": ldv}
 
@@ -337,8 +338,8 @@ def main():
         except Exception as exc:  # the baseline must not sink the GPU line
             cpu = {"value": None, "unit": "GNNZ-vec/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
-    # my kernels per step: pack + steps + reduce + mean + coefficients + series
-    gpu_launches = args.steps * (1 + launches + 1 + 1 + 1 + 1)
+    # my kernels per step: pack + recurrence steps + 2-stage reduce + mean + coefficients + series
+    gpu_launches = args.steps * (1 + launches + 2 + 1 + 1 + 1)
     line = {
         "metric": "Chebyshev moment steps: nnz*n_vec*deg/s (GNNZ-vec/s)",
         "value": value, "unit": "GNNZ-vec/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

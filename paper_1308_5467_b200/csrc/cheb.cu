@@ -420,14 +420,40 @@ __global__ void __launch_bounds__(kStepThreads) self_dot_kernel(StepArgs a) {
 }
 
 // ---- K2: partials -> per-probe moments ------------------------------------------
-__global__ void cheb_reduce_kernel(const double* __restrict__ partials, int64_t nblocks, int64_t ldv, int64_t n_vec,
+// Two fixed-order stages: (1) sums of kReduceChunk consecutive blocks per
+// (slot, chunk, column), coalesced over columns; (2) per (slot, probe) the sum
+// of the chunk sums in chunk order, then the doubling transform.  Deterministic.
+constexpr int kReduceChunk = 64;
+
+__global__ void cheb_reduce_stage1(const double* __restrict__ partials, int64_t nblocks, int64_t ldv, int64_t slots,
+                                   int64_t nchunks, double* __restrict__ stage) {
+  const int64_t total = slots * nchunks * ldv;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t l = idx % ldv, rest = idx / ldv;
+    const int64_t ch = rest % nchunks, k = rest / nchunks;
+    const int64_t b0 = ch * kReduceChunk, b1 = b0 + kReduceChunk < nblocks ? b0 + kReduceChunk : nblocks;
+    const double* p = partials + (k * nblocks + b0) * ldv + l;
+    double s = 0.0;
+    for (int64_t b = b0; b < b1; ++b, p += ldv) s += *p;
+    stage[idx] = s;
+  }
+}
+
+__global__ void cheb_reduce_stage2(const double* __restrict__ stage, int64_t nchunks, int64_t ldv, int64_t n_vec,
                                    int64_t degree, int mode, double* __restrict__ zeta_pp) {
   const int64_t total = n_vec * (degree + 1);
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
        idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = idx / n_vec, l = idx % n_vec;
-    double r = sum_blocks(partials, k, nblocks, ldv, l);
-    if (mode == SDB_CHEB_DOUBLING && k >= 2) r = 2.0 * r - sum_blocks(partials, k & 1, nblocks, ldv, l);
+    auto sum = [&](int64_t slot) {
+      const double* p = stage + slot * nchunks * ldv + l;
+      double s = 0.0;
+      for (int64_t ch = 0; ch < nchunks; ++ch) s += p[ch * ldv];
+      return s;
+    };
+    double r = sum(k);
+    if (mode == SDB_CHEB_DOUBLING && k >= 2) r = 2.0 * r - sum(k & 1);
     zeta_pp[l * (degree + 1) + k] = r;
   }
 }
@@ -596,6 +622,7 @@ static TilePlan plan_tile(const sdb_matrix* m, int64_t ldv, int mode) {
   const GridShapeTable tab = grid_shape_table(m->shape);
   for (int o = 0; o < tab.nt; ++o) p.t.wc[o] = o < m->nterms ? m->term_w_host[o] : 0.0;
   p.nblocks = (int64_t)p.t.n_xt * p.t.n_yt * p.t.n_zs;
+  if (p.nblocks > 8LL * num_sms(m->device)) return p;  // partials sized for <= 8 blocks per SM
   p.on = true;
   return p;
 }
@@ -637,10 +664,12 @@ static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
 static void cheb_layout(const sdb_matrix* m, int64_t ldv, int64_t degree, size_t* block_bytes,
                         size_t* partial_bytes) {
+  // partial_bytes covers the block partials plus the stage-1 reduce buffer
   *block_bytes = align256(sizeof(double) * (size_t)m->n * (size_t)ldv);
   // upper bound on step_blocks(): 8 resident 256-thread blocks per SM
   const int64_t bmax = 8LL * num_sms(m->device);
-  *partial_bytes = align256(sizeof(double) * (size_t)(degree + 1) * (size_t)bmax * (size_t)ldv);
+  const int64_t cmax = (bmax + kReduceChunk - 1) / kReduceChunk;
+  *partial_bytes = align256(sizeof(double) * (size_t)(degree + 1) * (size_t)(bmax + cmax) * (size_t)ldv);
 }
 
 // ---- step planning shared by the moment driver and the step-level ABI ------------
@@ -650,12 +679,14 @@ struct StepPlan {
   TilePlan tp;
   StepArgs a;   // n, ldv, nblocks, panel, slices, c, inv_d filled
   StencilView st;
+  int device;
 };
 
 static int plan_steps(const sdb_matrix* m, int64_t n_vec, int mode, double c, double d, StepPlan* P) {
   SDB_REQUIRE(n_vec >= 1 && n_vec <= SDB_MAX_BATCH, "n_vec must lie in [1, %d] per batch", SDB_MAX_BATCH);
   SDB_REQUIRE(mode == SDB_CHEB_DIRECT || mode == SDB_CHEB_DOUBLING, "unknown moment mode %d", mode);
   StepPlan& p = *P;
+  p.device = m->device;
   p.g = choose_geometry(n_vec);
   p.gk = p.g;
   p.a = StepArgs{};
@@ -724,10 +755,20 @@ static int launch_plan_step(const sdb_matrix* m, const StepPlan& P, int64_t degr
 
 static int launch_reduce(const StepPlan& P, int64_t n_vec, int64_t degree, int mode, const double* partials,
                          double* zeta_pp, cudaStream_t s) {
-  const int64_t total = n_vec * (degree + 1);
-  int blocks = (int)((total + 255) / 256);
-  if (blocks > 4096) blocks = 4096;
-  cheb_reduce_kernel<<<blocks, 256, 0, s>>>(partials, P.a.nblocks, P.g.ldv, n_vec, degree, mode, zeta_pp);
+  const int64_t nb = P.a.nblocks, ldv = P.g.ldv, slots = degree + 1;
+  const int64_t nch = (nb + kReduceChunk - 1) / kReduceChunk;
+  // stage buffer sits behind the largest possible partials array (cheb_layout)
+  const int64_t bmax = 8LL * num_sms(P.device);
+  double* stage = const_cast<double*>(partials) + slots * bmax * ldv;
+  const int64_t t1 = slots * nch * ldv;
+  int b1 = (int)((t1 + 255) / 256);
+  if (b1 > 65535) b1 = 65535;
+  cheb_reduce_stage1<<<b1, 256, 0, s>>>(partials, nb, ldv, slots, nch, stage);
+  SDB_CHECK_LAUNCH();
+  const int64_t t2 = n_vec * slots;
+  int b2 = (int)((t2 + 255) / 256);
+  if (b2 > 65535) b2 = 65535;
+  cheb_reduce_stage2<<<b2, 256, 0, s>>>(stage, nch, ldv, n_vec, degree, mode, zeta_pp);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
