@@ -30,7 +30,10 @@ struct TileArgs {
 };
 
 constexpr int kTileMaxX = 64;
-constexpr int kTileThreads = 256;
+#ifndef SDB_TILE_THREADS
+#define SDB_TILE_THREADS 256
+#endif
+constexpr int kTileThreads = SDB_TILE_THREADS;
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem);
