@@ -202,3 +202,56 @@ def rowpartition_moments(op, interval, degree, source, n_vec, mode=_native.SDB_C
         for sl in slabs:
             ghosted_probe_block(source, 0, n_vec, op.shape, sl.z0, sl.nzl, sl.ldv, sl.blocks[0])
         return run_rowpartition(slabs, plan, c, d, degree, mode, group if rank_of_slab else None, rank_of_slab)
+
+
+def prepare_rowpartition(op, interval, degree, source, n_vec, mode=_native.SDB_CHEB_DOUBLING, group=None,
+                         device=None, probes_host=None):
+    """Allocate this rank's slab (ghosted blocks, probes staged).  Returns
+    (slabs, plan, rank_of_slab); run with ``run_rowpartition``."""
+    import torch
+    import torch.distributed as dist
+
+    device = E.require_cuda(device)
+    nz = op.shape[2]
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    plan = SlabPlan(nz, world)
+    with torch.cuda.device(device):
+        sl = DeviceSlab(op, plan, rank, n_vec, degree, mode, device)
+        ghosted_probe_block(source, 0, n_vec, op.shape, sl.z0, sl.nzl, sl.ldv, sl.blocks[0])
+    return [sl], plan, ((lambda s: s) if world > 1 else None)
+
+
+def estimate_dos_rowpartition(op, interval, method, degree, source, n_vec, grid_points=200, product_formula=True,
+                              group=None, device=None):
+    """KPM DOS of a periodic stencil with the z-planes row-partitioned over the
+    ranks of ``group`` (collective; every rank returns the same estimate)."""
+    import torch
+
+    from .compare import GPU_METHODS
+    from .density import SpectralDensityEstimate, unit_grid
+    from .errors import NumericalFailure
+
+    if method not in ("kpm", "kpm-jackson"):
+        raise ValueError(f"row partition supports kpm / kpm-jackson (GPU methods: {GPU_METHODS})")
+    device = E.require_cuda(device)
+    mode = _native.SDB_CHEB_DOUBLING if product_formula else _native.SDB_CHEB_DIRECT
+    slabs, plan, ros = prepare_rowpartition(op, interval, degree, source, n_vec, mode, group, device)
+    zeta_pp = run_rowpartition(slabs, plan, float(interval.center), float(interval.halfwidth), degree, mode,
+                               group if ros else None, ros)
+    grid = unit_grid(grid_points)
+    zeta_dev, flag = E.mean_moments(zeta_pp, device)
+    damp = _native.SDB_DAMP_JACKSON if method == "kpm-jackson" else _native.SDB_DAMP_NONE
+    _, values, density = E.kpm_density_device(zeta_dev, degree, op.dim, damp, E.to_device(grid, device),
+                                              float(interval.halfwidth), device)
+    packed = torch.cat([zeta_dev, values, density, flag.to(torch.float64)]).cpu().numpy()
+    m1, g = degree + 1, len(grid)
+    if packed[-1] != 0.0 or not np.all(np.isfinite(packed[:m1])):
+        raise NumericalFailure(E.SPECTRUM_ESCAPE_HINT)
+    est = SpectralDensityEstimate.from_parts(grid, packed[m1:m1 + g], interval.from_unit(grid),
+                                             packed[m1 + g:m1 + 2 * g], interval, method=method,
+                                             params={"degree": degree, "moments": packed[:m1], "M": degree,
+                                                     "n_vec": n_vec, "slabs": plan.n_slabs})
+    if method == "kpm-jackson":
+        est.params["damping"] = "jackson"
+    return est
