@@ -130,6 +130,24 @@ def build_workload(config, fmt):
     return cfg, op, iv
 
 
+def kernel_label(op, dm):
+    from paper_1308_5467_b200 import _native
+
+    if dm.format != _native.SDB_FMT_STENCIL:
+        return "cheb_step_csr"
+    base = getattr(op, "offsets", None)
+    if base is None:
+        from paper_1308_5467_b200.operators import detect_stencil
+
+        st = detect_stencil(op.csr)
+        base = st.offsets if st is not None else []
+    if len(base) == 26:
+        return "cheb_step_tile (27-point box, 2.5-D shared-memory tiles)"
+    if len(base) == 6:
+        return "cheb_step_grid (7-point star, row panels)"
+    return "cheb_step_stencil"
+
+
 def nnz_of(op):
     return int(op.csr.nnz) if hasattr(op, "csr") and not hasattr(op, "offsets") else int(op.nnz)
 
@@ -362,7 +380,7 @@ def main():
                 ("stencil" if dm.format == _native.SDB_FMT_STENCIL else "csr"))
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic,
-            "kernel": "cheb_step_grid (7-point)" if dm.format == _native.SDB_FMT_STENCIL else "cheb_step_csr", "peak_source": f"{peak_kind} hbm_gbs",
+            "kernel": kernel_label(op, dm), "peak_source": f"{peak_kind} hbm_gbs",
             "bytes_per_launch": bytes_launch, "launches_per_step": launches,
             "avg_launch_us": avg_launch_s * 1e6, "kernel_share_of_step": k_ms / t_ms, "ldv": ldv}
 
