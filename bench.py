@@ -364,7 +364,8 @@ def main():
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt[0])
     e2e_value = units / e2e_s / 1e9
-    h2d = 8 * n * n_vec + 8 * cfg.grid_points
+    # probes (Rademacher: packed sign bits, 1/64 of the fp64 bytes) + the unit grid
+    h2d = (n_vec * ((n + 7) // 8) if cfg.probe_kind == "rademacher" else 8 * n * n_vec) + 8 * cfg.grid_points
     d2h = 8 * (cfg.degree + 1 + 2 * cfg.grid_points + 1)
 
     # ---- roofline of the dominant kernel (the fused recurrence step) ----
@@ -405,7 +406,8 @@ def main():
         "roofline": roof, "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "GNNZ-vec/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_s * 1e3,
-                "path": "estimate_dos(kpm-jackson) public API; probes from pinned host memory each step; "
+                "path": "estimate_dos(kpm-jackson) public API; probes from pinned host memory each step "
+                        "(Rademacher probes as packed sign bits, expanded to +-1.0 on the device); "
                         "matrix handle resident (uploaded once, cached per host object)"},
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),

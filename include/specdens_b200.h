@@ -133,6 +133,13 @@ SDB_API void sdb_matrix_destroy(sdb_matrix* m);
  * block is n x ldv (row-major, device; padding columns zeroed). */
 SDB_API int sdb_pack_probes(const double* probes_t, int64_t n_vec, int64_t n, int64_t ldv,
                     double* block, void* stream);
+/* Rademacher probes (stochastic.py:54: rng.integers(0, 2, dim) * 2.0 - 1.0) are
+ * exactly +-1: stage them as sign bits.  bits: device, n_vec rows of
+ * ceil(n/8) bytes, bit i of row l = (i >> 3, i & 7) little-endian (NumPy
+ * packbits bitorder='little'); 1 -> +1.0, 0 -> -1.0.  Writes the n x ldv
+ * block (padding columns zeroed). */
+SDB_API int sdb_unpack_signs(const uint8_t* bits, int64_t n_vec, int64_t n, int64_t ldv, double* block,
+                     void* stream);
 /* Inverse of sdb_pack_probes for the first n_vec columns. */
 SDB_API int sdb_unpack_block(const double* block, int64_t n, int64_t ldv, int64_t n_vec,
                      double* out_t, void* stream);

@@ -77,6 +77,7 @@ SIGNATURES = {
     "sdb_matrix_destroy": (None, [_p]),
     "sdb_pack_probes": (_i, [_p, _i64, _i64, _i64, _p, _p]),
     "sdb_unpack_block": (_i, [_p, _i64, _i64, _i64, _p, _p]),
+    "sdb_unpack_signs": (_i, [_p, _i64, _i64, _i64, _p, _p]),
     "sdb_cheb_workspace_size": (_i, [_p, _i64, _i64, _i, ctypes.POINTER(_sz)]),
     "sdb_cheb_moments": (_i, [_p, _d, _d, _i64, _i64, _i, _p, _p, _p, _sz, _p, ctypes.POINTER(ctypes.c_float)]),
     "sdb_cheb_partials_size": (_i, [_p, _i64, _i64, _i, ctypes.POINTER(_sz)]),

@@ -155,6 +155,26 @@ __global__ void unpack_kernel(const double* __restrict__ block, int64_t n, int64
   }
 }
 
+// one thread per (row, 2 columns): coalesced double2 stores into the block
+__global__ void unpack_signs_kernel(const uint8_t* __restrict__ bits, int64_t n_vec, int64_t n, int64_t ldv,
+                                    double* __restrict__ block) {
+  const int64_t nbytes = (n + 7) / 8;
+  const int64_t half = ldv / 2;
+  const int64_t total = n * half;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / half, c = 2 * (idx % half);
+    double v[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t l = c + u;
+      v[u] = 0.0;
+      if (l < n_vec) v[u] = ((bits[l * nbytes + (i >> 3)] >> (i & 7)) & 1) ? 1.0 : -1.0;
+    }
+    *reinterpret_cast<double2*>(block + i * ldv + c) = make_double2(v[0], v[1]);
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -373,6 +393,17 @@ int sdb_pack_probes(const double* probes_t, int64_t n_vec, int64_t n, int64_t ld
   SDB_REQUIRE(n_vec >= 1 && n >= 1 && ldv >= n_vec, "bad pack shape");
   dim3 grid((unsigned)((n + 31) / 32), (unsigned)((ldv + 31) / 32));
   pack_kernel<<<grid, dim3(32, 8), 0, (cudaStream_t)stream>>>(probes_t, n_vec, n, ldv, block);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+int sdb_unpack_signs(const uint8_t* bits, int64_t n_vec, int64_t n, int64_t ldv, double* block, void* stream) {
+  SDB_REQUIRE(bits && block, "NULL argument");
+  SDB_REQUIRE(n_vec >= 1 && n >= 1 && ldv >= n_vec && ldv % 2 == 0, "bad unpack shape");
+  const int64_t total = n * (ldv / 2);
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 65535 * 4) blocks = 65535 * 4;
+  unpack_signs_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(bits, n_vec, n, ldv, block);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

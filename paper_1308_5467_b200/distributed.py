@@ -60,6 +60,9 @@ class _ShiftedSource:
 
     def __init__(self, src, start):
         self.src, self.start, self.dim = src, start, src.dim
+        self.kind = getattr(src, "kind", None)
+        if hasattr(src, "draw_block_signs"):
+            self.draw_block_signs = lambda s, c: src.draw_block_signs(self.start + s, c)
 
     def draw(self, i):
         return self.src.draw(self.start + i)

@@ -79,12 +79,20 @@ def stage_probes(source, start, count, n, device, stream):
     torch = _torch()
     if int(source.dim) != n:
         raise ValueError(f"probe dimension {source.dim} does not match operator dimension {n}")
+    ldv = block_ldv(count)
+    if getattr(source, "kind", None) == "rademacher" and hasattr(source, "draw_block_signs"):
+        bits = source.draw_block_signs(start, count)
+        dev_b = torch.empty(bits.shape, dtype=torch.uint8, device=device)
+        dev_b.copy_(bits, non_blocking=True)
+        block = torch.empty((n, ldv), dtype=torch.float64, device=device)
+        _native.call("sdb_unpack_signs", ptr(dev_b), count, n, ldv, ptr(block), stream)
+        block._sdb_keepalive = (bits, dev_b)
+        return Staged(block=block, ldv=ldv, h2d_bytes=int(bits.numel()))
     host = draw_block(source, start, count)
     if not isinstance(host, torch.Tensor):
         host = torch.from_numpy(np.ascontiguousarray(host, dtype=np.float64))
     dev_t = torch.empty((count, n), dtype=torch.float64, device=device)
     dev_t.copy_(host, non_blocking=True)
-    ldv = block_ldv(count)
     block = torch.empty((n, ldv), dtype=torch.float64, device=device)
     _native.call("sdb_pack_probes", ptr(dev_t), count, n, ldv, ptr(block), stream)
     # keep the host buffer alive until the stream has consumed it

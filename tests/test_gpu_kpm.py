@@ -321,3 +321,22 @@ def test_tile_kernel_variants_match_oracle(monkeypatch, tile, dims, shape):
     est = sdb.estimate_dos(op, iv, "kpm-jackson", 37, src, 32, grid_points=300, product_formula=True)
     _, dens = O.evaluate_kpm_dos(O.moments_to_coefficients(ref, n, "jackson"), iv.halfwidth, grid)
     assert np.max(np.abs(est.density - dens)) <= DOS_ATOL
+
+
+def test_rademacher_sign_staging_is_exact():
+    """Sign-bit staging of Rademacher probes gives bit-identical moments to fp64 staging."""
+
+    class PlainSource:  # the reference's protocol only: draw(l) and dim
+        def __init__(self, src):
+            self.src, self.dim = src, src.dim
+
+        def draw(self, i):
+            return self.src.draw(i)
+
+    op = W.anderson_3d(12)
+    iv = W.gershgorin_interval(op)
+    src = sdb.ProbeVectorSource("rademacher", seed=9, dim=op.dim)
+    mapped = sdb.apply_spectral_map(op, iv)
+    a = sdb.moments_via_product_formula(mapped, 40, src, 33)
+    b = sdb.moments_via_product_formula(mapped, 40, PlainSource(src), 33)
+    np.testing.assert_array_equal(a.zeta, b.zeta)

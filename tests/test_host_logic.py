@@ -170,3 +170,14 @@ def test_detect_stencil_on_host():
     st = detect_stencil(W.anderson_3d(9).csr)
     assert st is not None and st.shape == (9, 9, 9)
     assert detect_stencil(W.build_matrix("C1").csr) is None
+
+
+def test_rademacher_sign_bits_round_trip():
+    src = sdb.ProbeVectorSource("rademacher", seed=3, dim=1001, stream=2)
+    bits = np.asarray(src.draw_block_signs(5, 4))
+    assert bits.shape == (4, 126)
+    for i in range(4):
+        v = np.unpackbits(bits[i], bitorder="little")[:1001] * 2.0 - 1.0
+        np.testing.assert_array_equal(v, src.draw(5 + i))
+    with pytest.raises(ValueError):
+        sdb.ProbeVectorSource("gaussian", 0, 10).draw_block_signs(0, 1)
