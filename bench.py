@@ -57,13 +57,14 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
-def load_traffic(config, fmt):
+def load_traffic(config, fmt, kernel):
+    """ncu DRAM bytes (read + write) of one step launch, per config/format/kernel."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    v = d.get(f"{config}:{fmt}")
+    v = d.get(f"{config}:{fmt}:{kernel}")
     return None if v is None else float(v)
 
 
@@ -130,22 +131,16 @@ def build_workload(config, fmt):
     return cfg, op, iv
 
 
-def kernel_label(op, dm):
+def kernel_label(dm, n_vec, mode):
+    """Name of the step kernel the library runs (sdb_cheb_kernel)."""
     from paper_1308_5467_b200 import _native
 
-    if dm.format != _native.SDB_FMT_STENCIL:
-        return "cheb_step_csr"
-    base = getattr(op, "offsets", None)
-    if base is None:
-        from paper_1308_5467_b200.operators import detect_stencil
-
-        st = detect_stencil(op.csr)
-        base = st.offsets if st is not None else []
-    if len(base) == 26:
-        return "cheb_step_tile (27-point box, 2.5-D shared-memory tiles)"
-    if len(base) == 6:
-        return "cheb_step_grid (7-point star, row panels)"
-    return "cheb_step_stencil"
+    name = _native.load().sdb_cheb_kernel(dm.handle, n_vec, mode).decode()
+    detail = {"cheb_step_zmarch": "TMA z-march, ghost-padded planes, register-rolled z terms",
+              "cheb_step_tile": "2.5-D cp.async shared-memory tiles",
+              "cheb_step_grid": "row panels", "cheb_step_csr": "CSR row groups",
+              "cheb_step_stencil": "generic stencil"}.get(name, "")
+    return f"{name} ({detail})" if detail else name
 
 
 def nnz_of(op):
@@ -376,12 +371,15 @@ def main():
     avg_launch_s = k_ms * 1e-3 / launches
     achieved = bytes_launch / avg_launch_s / 1e9
     peak, peak_kind = load_peaks()
-    traffic = load_traffic(args.config, args.format)
+    mode_c = _native.SDB_CHEB_DOUBLING if product else _native.SDB_CHEB_DIRECT
+    klabel = kernel_label(dm, n_vec, mode_c)
+    kname = klabel.split(" ")[0]
+    traffic = load_traffic(args.config, args.format, kname)
     internal = ("stencil (detected from CSR)" if dm.detected_stencil else
                 ("stencil" if dm.format == _native.SDB_FMT_STENCIL else "csr"))
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "traffic": traffic,
-            "kernel": kernel_label(op, dm), "peak_source": f"{peak_kind} hbm_gbs",
+            "kernel": klabel, "peak_source": f"{peak_kind} hbm_gbs",
             "bytes_per_launch": bytes_launch, "launches_per_step": launches,
             "avg_launch_us": avg_launch_s * 1e6, "kernel_share_of_step": k_ms / t_ms, "ldv": ldv}
 
@@ -393,7 +391,8 @@ def main():
             cpu = {"value": None, "unit": "GNNZ-vec/s", "cores": 1, "kind": "port", "sample": f"failed: {exc}"}
 
     # my kernels per step: pack + recurrence steps + 2-stage reduce + mean + coefficients + series
-    gpu_launches = args.steps * (1 + launches + 2 + 1 + 1 + 1)
+    # (+1 ghost-padding copy of the probes on the z-march path)
+    gpu_launches = args.steps * (1 + launches + 2 + 1 + 1 + 1 + (1 if kname == "cheb_step_zmarch" else 0))
     line = {
         "metric": "Chebyshev moment steps: nnz*n_vec*deg/s (GNNZ-vec/s)",
         "value": value, "unit": "GNNZ-vec/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

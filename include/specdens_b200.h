@@ -156,6 +156,10 @@ SDB_API int sdb_cheb_workspace_size(const sdb_matrix* m, int64_t n_vec, int64_t 
 SDB_API int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree,
                      int mode, const double* probes, double* zeta_pp, void* workspace,
                      size_t workspace_bytes, void* stream, float* step_ms);
+/* Name of the step kernel sdb_cheb_moments runs for this matrix / probe count /
+ * mode ("cheb_step_zmarch", "cheb_step_grid", "cheb_step_tile",
+ * "cheb_step_stencil" or "cheb_step_csr"); "" for invalid arguments. */
+SDB_API const char* sdb_cheb_kernel(const sdb_matrix* m, int64_t n_vec, int mode);
 /* Step-level form of sdb_cheb_moments for callers that exchange data between
  * steps (row-partitioned multi-GPU: halo planes).  Step k reads x = w_k,
  * prev = w_{k-1} (k >= 1), v0 (direct mode), writes next = w_{k+1} (may alias

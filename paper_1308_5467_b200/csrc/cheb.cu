@@ -18,7 +18,7 @@
 // warp -> block in a fixed order and writes one partial per (slot, block,
 // column).  K2 sums those partials over blocks in index order: no atomics, so
 // results are bitwise reproducible.
-#include "rowgroup.cuh"
+#include "stepargs.cuh"
 
 namespace sdb {
 
@@ -43,23 +43,7 @@ __host__ __device__ constexpr int step_min_blocks(int l, int vpl) {
   return l < 8 ? (vpl == 1 ? 4 : 2) : (vpl == 1 ? SDB_MINB_V1 : (vpl == 2 ? SDB_MINB_V2 : 2));
 }
 
-struct StepArgs {
-  const double* x;     // w_k                      (gathered)
-  const double* prev;  // w_{k-1}                  (row-local; may alias next)
-  double* next;        // w_{k+1}
-  const double* v0;    // probes (direct mode dots)
-  double c;            // spectral centre
-  double inv_d;        // 1/halfwidth
-  int64_t n;
-  int64_t ldv;
-  int64_t nblocks;
-  int64_t panel;       // rows per panel of the phased schedule
-  double* partials;    // [(M+1)][nblocks][ldv]
-  int slotA;           // doubling: <w+,w+>, direct: <v0,w+>   (-1: none)
-  int slotB;           // doubling: <w+,w>                       (-1: none)
-  int slot0;           // step 0: <w0,w0>                        (-1: none)
-  int slices;          // column slices per panel (grid kernel; 1 = whole rows)
-};
+
 
 // Epilogue shared by the CSR and stencil steps, split in two so the row's own
 // operands (x_i for the spectral shift, w_{k-1}, v_0) are requested before
@@ -284,23 +268,6 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
 // is the sorted-column order of the stencil's CSR form for nx, ny >= 3.  Per
 // row the wrapped neighbour offsets along each axis are computed once; a
 // term's column is then row + xo + yo + zo.
-template <int SHAPE>
-struct GridShape;
-template <>
-struct GridShape<SDB_SHAPE_FACE7> {
-  static constexpr int NT = 7;
-  __host__ __device__ static constexpr int dx(int o) { return o == 2 ? -1 : (o == 4 ? 1 : 0); }
-  __host__ __device__ static constexpr int dy(int o) { return o == 1 ? -1 : (o == 5 ? 1 : 0); }
-  __host__ __device__ static constexpr int dz(int o) { return o == 0 ? -1 : (o == 6 ? 1 : 0); }
-};
-template <>
-struct GridShape<SDB_SHAPE_BOX27> {
-  static constexpr int NT = 27;
-  __host__ __device__ static constexpr int dx(int o) { return o % 3 - 1; }
-  __host__ __device__ static constexpr int dy(int o) { return (o / 3) % 3 - 1; }
-  __host__ __device__ static constexpr int dz(int o) { return o / 9 - 1; }
-};
-
 struct GridShapeTable {
   int nt;
 };
@@ -787,8 +754,23 @@ int sdb_cheb_workspace_size(const sdb_matrix* m, int64_t n_vec, int64_t degree, 
   Geometry g = choose_geometry(n_vec);
   size_t bb, pb;
   cheb_layout(m, g.ldv, degree, &bb, &pb);
-  *bytes = 2 * bb + pb;
+  ZmPlan zp;
+  int rc = zm_plan(m, g.ldv, mode, &zp);
+  if (rc) return rc;
+  // z-march path: padded probe copy + two padded recurrence buffers
+  *bytes = zp.on ? 3 * zp.block_bytes + pb : 2 * bb + pb;
   return SDB_OK;
+}
+
+const char* sdb_cheb_kernel(const sdb_matrix* m, int64_t n_vec, int mode) {
+  if (!m || n_vec < 1 || n_vec > SDB_MAX_BATCH) return "";
+  const Geometry g = choose_geometry(n_vec);
+  ZmPlan zp;
+  if (zm_plan(m, g.ldv, mode, &zp) == SDB_OK && zp.on) return zp.name;
+  if (m->format == SDB_FMT_CSR) return "cheb_step_csr";
+  if (plan_tile(m, g.ldv, mode).on) return "cheb_step_tile";
+  if (m->shape == SDB_SHAPE_FACE7 || m->shape == SDB_SHAPE_BOX27) return "cheb_step_grid";
+  return "cheb_step_stencil";
 }
 
 int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode,
@@ -808,25 +790,54 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
   if ((rc = plan_steps(m, n_vec, mode, c, d, &P))) return rc;
   size_t bb, pb;
   cheb_layout(m, P.g.ldv, degree, &bb, &pb);
-  double* bufA = (double*)workspace;
-  double* bufB = (double*)((char*)workspace + bb);
-  double* partials = (double*)((char*)workspace + 2 * bb);
-
+  ZmPlan zp;
+  if ((rc = zm_plan(m, P.g.ldv, mode, &zp))) return rc;
   const int64_t steps = (mode == SDB_CHEB_DOUBLING) ? (degree + 1) / 2 : degree;
+  if (steps == 0) zp.on = false;  // degree 0: only <v0, v0>
+  const size_t blk = zp.on ? zp.block_bytes : bb;
+  double* bufA = (double*)workspace;
+  double* bufB = (double*)((char*)workspace + blk);
+  double* padded = zp.on ? (double*)((char*)workspace + 2 * blk) : nullptr;
+  double* partials = (double*)((char*)workspace + (zp.on ? 3 : 2) * blk);
+
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (step_ms) {
     SDB_CUDA(cudaEventCreate(&e0));
     SDB_CUDA(cudaEventCreate(&e1));
     SDB_CUDA(cudaEventRecord(e0, s));
   }
-  const double* cur = probes;
+  const double* v0 = probes;
+  if (zp.on) {  // ghost-padded copy of the probes (counted in the step time)
+    if ((rc = zm_pad(m, probes, P.g.ldv, padded, s))) return rc;
+    v0 = padded;
+  }
+  const double* cur = v0;
   const double* prev = nullptr;
   for (int64_t k = 0; k < (steps > 0 ? steps : 1); ++k) {
     double* next = (k == 0) ? bufA : (k == 1 ? bufB : const_cast<double*>(prev));
-    if ((rc = launch_plan_step(m, P, degree, mode, k, cur, prev, next, probes, partials, s))) return rc;
+    if (zp.on) {
+      StepArgs a = P.a;
+      a.partials = partials;
+      a.v0 = v0;
+      a.x = cur;
+      a.prev = prev;
+      a.next = next;
+      a.slot0 = (k == 0) ? 0 : -1;
+      if (mode == SDB_CHEB_DOUBLING) {
+        a.slotB = (2 * k + 1 <= degree) ? (int)(2 * k + 1) : -1;
+        a.slotA = (2 * k + 2 <= degree) ? (int)(2 * k + 2) : -1;
+      } else {
+        a.slotA = (int)(k + 1);
+        a.slotB = -1;
+      }
+      if ((rc = zm_launch_step(m, zp, a, k == 0, mode, s))) return rc;
+    } else if ((rc = launch_plan_step(m, P, degree, mode, k, cur, prev, next, probes, partials, s))) {
+      return rc;
+    }
     prev = cur;
     cur = next;
   }
+  if (zp.on) P.a.nblocks = zp.nbp;  // partial rows the reduce sums
   if (step_ms) SDB_CUDA(cudaEventRecord(e1, s));
   if ((rc = launch_reduce(P, n_vec, degree, mode, partials, zeta_pp, s))) return rc;
   if (step_ms) {

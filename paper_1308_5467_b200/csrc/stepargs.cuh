@@ -1,0 +1,69 @@
+// stepargs.cuh — step-kernel argument block and compile-time grid shapes,
+// shared by cheb.cu (row-panel / tile kernels) and zmarch.cu (TMA z-march).
+#pragma once
+#include "rowgroup.cuh"
+
+namespace sdb {
+
+struct StepArgs {
+  const double* x;     // w_k                      (gathered)
+  const double* prev;  // w_{k-1}                  (row-local; may alias next)
+  double* next;        // w_{k+1}
+  const double* v0;    // probes (direct mode dots)
+  double c;            // spectral centre
+  double inv_d;        // 1/halfwidth
+  int64_t n;
+  int64_t ldv;
+  int64_t nblocks;
+  int64_t panel;       // rows per panel of the phased schedule
+  double* partials;    // [(M+1)][nblocks][ldv]
+  int slotA;           // doubling: <w+,w+>, direct: <v0,w+>   (-1: none)
+  int slotB;           // doubling: <w+,w>                       (-1: none)
+  int slot0;           // step 0: <w0,w0>                        (-1: none)
+  int slices;          // column slices per panel (grid kernel; 1 = whole rows)
+};
+
+// Structured-grid term order (7-point faces, 27-point box): lexicographic in
+// (dz, dy, dx), which is the sorted-column order of the stencil's CSR form for
+// nx, ny >= 3.
+template <int SHAPE>
+struct GridShape;
+template <>
+struct GridShape<SDB_SHAPE_FACE7> {
+  static constexpr int NT = 7;
+  __host__ __device__ static constexpr int dx(int o) { return o == 2 ? -1 : (o == 4 ? 1 : 0); }
+  __host__ __device__ static constexpr int dy(int o) { return o == 1 ? -1 : (o == 5 ? 1 : 0); }
+  __host__ __device__ static constexpr int dz(int o) { return o == 0 ? -1 : (o == 6 ? 1 : 0); }
+};
+template <>
+struct GridShape<SDB_SHAPE_BOX27> {
+  static constexpr int NT = 27;
+  __host__ __device__ static constexpr int dx(int o) { return o % 3 - 1; }
+  __host__ __device__ static constexpr int dy(int o) { return (o / 3) % 3 - 1; }
+  __host__ __device__ static constexpr int dz(int o) { return o / 9 - 1; }
+};
+
+
+// ---- TMA z-march path (zmarch.cu) ------------------------------------------------
+// Plan for sdb_cheb_moments on a periodic 7/27-point grid: the recurrence
+// buffers are ghost-padded blocks [nz][ny+2][nx+2][ldv] (zm_block_bytes each).
+struct ZmPlan {
+  bool on = false;
+  int cfg = -1;          // tile configuration (CS, TX, TY, PPT)
+  int CS = 0, TX = 0, TY = 0;
+  int R = 0;             // ring slots
+  int ZS = 0, n_zs = 0;  // planes per z segment, segments
+  int64_t items = 0;     // work items (tile x slice x z segment)
+  int64_t grid = 0;      // persistent blocks (multiple of the slice count)
+  int64_t nbp = 0;       // partial rows = grid / slices
+  size_t smem = 0;
+  size_t block_bytes = 0;
+  const char* name = "";
+};
+int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* p);
+// w_{k+1} = step(x = w_k, prev = w_{k-1}) on padded blocks; partial rows p.nbp.
+int zm_launch_step(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, bool first, int mode, cudaStream_t s);
+// probes (n x ldv) -> padded block
+int zm_pad(const sdb_matrix* m, const double* probes, int64_t ldv, double* padded, cudaStream_t s);
+
+}  // namespace sdb

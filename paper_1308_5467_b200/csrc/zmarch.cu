@@ -1,0 +1,598 @@
+// zmarch.cu — TMA z-marching Chebyshev step for periodic 7-point / 27-point
+// grids (both moment modes); used by sdb_cheb_moments (cheb.cu) when it applies.
+//
+// Why: with 64 probes one grid point of the probe block is 512 B.  The
+// row-panel kernel (cheb_step_grid) gathers every neighbour through L2
+// (~1.15 GB of L2->SM traffic per C2 step, capped by L2 throughput), and the
+// cp.async tile kernel (tile25d.cuh) spends its time issuing 16-byte copies
+// and waiting at block barriers.  Here:
+//
+//  * the recurrence buffers use a ghost-padded layout
+//      [nz][ny+2][nx+2][ldv]   (one periodic ghost layer in x and y)
+//    so the (TY+2) x (TX+2) halo tile of a plane, CS probe columns wide, is
+//    ONE rectangular TMA box (cp.async.bulk.tensor.4d), whatever the tile's
+//    position on the torus; the epilogue writes the ghost copies of boundary
+//    points (1.6 % extra stores at 256^2 planes, 6 % at 64^2);
+//  * one producer warp streams the planes of the block's z-segment through a
+//    ring of R shared-memory slots (mbarrier full/empty pairs, expect_tx), so
+//    the consumer warps never execute a block-wide barrier;
+//  * each consumer thread owns PPT (x, y) columns x one probe pair and marches
+//    z with three rolling register accumulators: plane p is read from shared
+//    memory ONCE (9 or 5 loads per point) and contributes its dz = -1 terms to
+//    out(p+1), its dz = 0 terms to out(p) and its dz = +1 terms to out(p-1),
+//    which is then complete.  Per output point the FMAs therefore run in
+//    lexicographic (dz, dy, dx) order -- the same sequence as cheb_step_grid,
+//    so both kernels produce bit-identical w_{k+1};
+//  * the slot is released right after the loads (values live in registers);
+//    w_{k-1}, v_0 and the diagonal of the next plane are prefetched into
+//    registers one plane ahead with evict-first loads.
+//
+// Per point the epilogue is the grid kernel's: (y - c x)/d, 2 t - w_{k-1},
+// store, and the moment dots of the step (doubling <w+,w+>, <w+,w>; direct
+// <v0,w+>; + <w0,w0> on the first step).  Partials: block b owns the CS
+// columns of slice b % slices of partial row b / slices (fixed order).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <mutex>
+#include <type_traits>
+
+#include "stepargs.cuh"
+
+namespace sdb {
+
+struct ZmArgs {
+  int nx, ny, nz;
+  int n_xt, n_yt, n_zs, ZS;   // tiles in x, y; z segments and planes per segment
+  int slices;                 // ldv / CS
+  int R;                      // ring slots
+  int64_t items;              // n_xt * n_yt * n_zs * slices
+  const double* diag;         // n (unpadded)
+  double wc[27];              // weights, lexicographic (dz, dy, dx); centre unused
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred P1;\n"
+      "ZM_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra ZM_WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
+                                            int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// Streamed rows (w_{k-1}, v0 reads; w_{k+1} writes): cache-streaming hints.
+__device__ __forceinline__ double2 ld_d2_cs(const double* p) {
+  double2 r;
+  asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_d2_cs(double* p, double2 v) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// Which in-plane positions (dy, dx) a shape reads: bit (dy+1)*3 + (dx+1).
+template <int SHAPE>
+__host__ __device__ constexpr int zm_plane_mask() {
+  int m = 0;
+  for (int o = 0; o < GridShape<SHAPE>::NT; ++o)
+    m |= 1 << ((GridShape<SHAPE>::dy(o) + 1) * 3 + GridShape<SHAPE>::dx(o) + 1);
+  return m;
+}
+
+template <int CS, int TX, int TY, int PPT>
+struct ZmGeom {
+  static constexpr int L = CS / 2;                 // lanes per point (one double2 each)
+  static constexpr int NT = TX * TY * L / PPT;     // consumer threads
+  static constexpr int GROUPS = NT / L;            // points per pass
+  static constexpr int PX = TX + 2, PY = TY + 2;   // halo box extent
+  static constexpr int BOX = PY * PX * CS;         // doubles per plane box
+  static_assert((TX * TY) % GROUPS == 0, "tile must split evenly over the point groups");
+  static_assert(NT % 32 == 0 && NT <= 1024 - 32, "consumer threads");
+};
+
+// Shared-memory ring slot: the halo box of x = w_k (always), then for output
+// planes the interior boxes of w_{k-1} (not on the first step), v0 (direct
+// mode after the first step) and the diagonal.
+template <int CS, int TX, int TY, int MODE, bool FIRST>
+struct ZmSlot {
+  static constexpr int XB = (TY + 2) * (TX + 2) * CS;                            // x halo box
+  static constexpr int PB = FIRST ? 0 : TY * TX * CS;                            // w_{k-1}
+  static constexpr int VB = (MODE == SDB_CHEB_DIRECT && !FIRST) ? TY * TX * CS : 0;  // v0
+  static constexpr int DB = TY * TX;                                             // diagonal
+  static constexpr int X0 = 0, P0 = (XB + 15) / 16 * 16, V0 = P0 + (PB + 15) / 16 * 16,
+                       D0 = V0 + (VB + 15) / 16 * 16;
+  static constexpr int DOUBLES = D0 + (DB + 15) / 16 * 16;  // 128-byte aligned pieces
+  static constexpr uint32_t HALO_BYTES = XB * 8;
+  static constexpr uint32_t FULL_BYTES = (XB + PB + VB + DB) * 8;
+};
+
+struct ZmMaps {
+  CUtensorMap x, prev, v0, diag;
+};
+
+template <int SHAPE, int CS, int TX, int TY, int PPT, int MODE, bool FIRST>
+__global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
+    cheb_step_zmarch(const __grid_constant__ ZmMaps maps, ZmArgs t, StepArgs a) {
+  using G = GridShape<SHAPE>;
+  using Z = ZmGeom<CS, TX, TY, PPT>;
+  using SL = ZmSlot<CS, TX, TY, MODE, FIRST>;
+  constexpr int L = Z::L, NT = Z::NT, GROUPS = Z::GROUPS;
+  constexpr int PMASK = zm_plane_mask<SHAPE>();
+  extern __shared__ __align__(128) double zsm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(zsm + (int64_t)t.R * SL::DOUBLES);
+  uint64_t* empty = full + t.R;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  if (tid == 0) {
+    for (int s = 0; s < t.R; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, NT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int nx = t.nx, ny = t.ny, nz = t.nz;
+  const int64_t pstride_y = (int64_t)(nx + 2) * a.ldv;  // padded row of points
+  const int64_t pplane = (int64_t)(ny + 2) * pstride_y;  // padded plane
+  const int64_t G_ = gridDim.x;
+
+  if (tid >= NT) {
+    // ---- producer warp: one elected lane streams the plane groups ----
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.x) : "memory");
+      int s = 0;
+      uint32_t use = 0;
+      for (int64_t item = blockIdx.x; item < t.items; item += G_) {
+        const int slice = (int)(item % t.slices);
+        int64_t sp = item / t.slices;
+        const int xt = (int)(sp % t.n_xt);
+        sp /= t.n_xt;
+        const int yt = (int)(sp % t.n_yt);
+        const int zs = (int)(sp / t.n_yt);
+        const int zbeg = zs * t.ZS, zend = min(zbeg + t.ZS, nz);
+        const int c0 = slice * CS, x0 = xt * TX, y0 = yt * TY;
+        for (int p = zbeg - 1; p <= zend; ++p) {
+          if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
+          const int zw = p < 0 ? p + nz : (p >= nz ? p - nz : p);
+          const bool outp = p >= zbeg && p < zend;
+          double* slot = zsm + (int64_t)s * SL::DOUBLES;
+          mbar_expect_tx(full + s, outp ? SL::FULL_BYTES : SL::HALO_BYTES);
+          tma_load_4d(slot + SL::X0, &maps.x, full + s, c0, x0, y0, zw);
+          if (outp) {
+            if (SL::PB) tma_load_4d(slot + SL::P0, &maps.prev, full + s, c0, x0 + 1, y0 + 1, p);
+            if (SL::VB) tma_load_4d(slot + SL::V0, &maps.v0, full + s, c0, x0 + 1, y0 + 1, p);
+            tma_load_3d(slot + SL::D0, &maps.diag, full + s, x0, y0, p);
+          }
+          if (++s == t.R) {
+            s = 0;
+            ++use;
+          } 
+        }
+      }
+    }
+    return;
+  }
+
+  // ---- consumer threads ----
+  const int q = tid % L, g = tid / L;
+  double2 accA = make_double2(0.0, 0.0), accB = accA, accZ = accA;
+  int s = 0;           // ring slot of the next plane
+  uint32_t phase = 0;  // its full-barrier parity
+  int pb_row = -1;     // partial row of this block (fixed slice: gridDim % slices == 0)
+  int col0 = 0;
+  for (int64_t item = blockIdx.x; item < t.items; item += G_) {
+    const int slice = (int)(item % t.slices);
+    int64_t sp = item / t.slices;
+    const int xt = (int)(sp % t.n_xt);
+    sp /= t.n_xt;
+    const int yt = (int)(sp % t.n_yt);
+    const int zs = (int)(sp / t.n_yt);
+    const int zbeg = zs * t.ZS, zend = min(zbeg + t.ZS, nz);
+    col0 = slice * CS;
+    pb_row = (int)(blockIdx.x / t.slices);
+    // this thread's columns: point index g + k*GROUPS of the TX x TY tile
+    int cx[PPT], cy[PPT], xo[PPT], io[PPT], dio[PPT];
+    int64_t cofs[PPT];  // padded block offset of (z = zbeg, y, x) + column
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+      const int pnt = g + k * GROUPS;
+      const int px = pnt % TX, py = pnt / TX;
+      cx[k] = xt * TX + px;
+      cy[k] = yt * TY + py;
+      xo[k] = ((py + 1) * (TX + 2) + (px + 1)) * CS + 2 * q;  // centre in the x halo box
+      io[k] = (py * TX + px) * CS + 2 * q;                    // in the interior boxes
+      dio[k] = py * TX + px;                                  // in the diagonal box
+      cofs[k] = (int64_t)zbeg * pplane + (int64_t)(cy[k] + 1) * pstride_y + (int64_t)(cx[k] + 1) * a.ldv + col0 +
+                2 * q;
+    }
+    // rolling accumulators: at plane p, accC = out(p), accN = out(p+1), accP = out(p-1)
+    double2 accN[PPT], accC[PPT], accP[PPT];
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) accN[k] = accC[k] = accP[k] = make_double2(0.0, 0.0);
+    double* pn = a.next - 2 * pplane;  // output plane p - 1 (+ cofs), for p = zbeg - 1 first
+    int sprev = -1;  // slot of plane p - 1 (this item), released after its epilogue
+    for (int p = zbeg - 1; p <= zend; ++p) {
+      mbar_wait(full + s, phase);
+      const double* slot = zsm + (int64_t)s * SL::DOUBLES;
+      const bool outp = p >= zbeg && p < zend;
+      // plane p: per column, the 3x3 (or star) neighbourhood into registers,
+      // then its terms in lexicographic (dz, dy, dx) order
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        const double dg = outp ? slot[SL::D0 + dio[k]] : 0.0;
+        double2 nb[9];
+#pragma unroll
+        for (int e = 0; e < 9; ++e) {
+          if (!((PMASK >> e) & 1)) continue;
+          const int dy = e / 3 - 1, dx = e % 3 - 1;
+          nb[e] = *reinterpret_cast<const double2*>(slot + SL::X0 + xo[k] + (dy * (TX + 2) + dx) * CS);
+        }
+#pragma unroll
+        for (int o = 0; o < G::NT; ++o) {
+          const int e = (G::dy(o) + 1) * 3 + G::dx(o) + 1;
+          const double2 v = nb[e];
+          const bool centre = G::dx(o) == 0 && G::dy(o) == 0 && G::dz(o) == 0;
+          const double w = centre ? dg : t.wc[o];
+          double2& y = G::dz(o) < 0 ? accN[k] : (G::dz(o) == 0 ? accC[k] : accP[k]);
+          y.x = fma(w, v.x, y.x);
+          y.y = fma(w, v.y, y.y);
+        }
+      }
+      // out(p-1) is complete: its operands are in the previous slot
+      if (p - 1 >= zbeg) {
+        const double* ps = zsm + (int64_t)sprev * SL::DOUBLES;
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const double2 xi = *reinterpret_cast<const double2*>(ps + SL::X0 + xo[k]);
+          const double tx = (accP[k].x - a.c * xi.x) * a.inv_d;
+          const double ty = (accP[k].y - a.c * xi.y) * a.inv_d;
+          double2 wn;
+          if (FIRST) {
+            wn = make_double2(tx, ty);
+          } else {
+            const double2 wp = *reinterpret_cast<const double2*>(ps + SL::P0 + io[k]);
+            wn = make_double2(2.0 * tx - wp.x, 2.0 * ty - wp.y);
+          }
+          double* dst = pn + cofs[k];
+          st_d2_cs(dst, wn);
+          // periodic ghost copies (x, y and the corner)
+          const int gx = cx[k] == 0 ? nx : (cx[k] == nx - 1 ? -nx : 0);
+          const int gy = cy[k] == 0 ? ny : (cy[k] == ny - 1 ? -ny : 0);
+          if (gx) st_d2_cs(dst + (int64_t)gx * a.ldv, wn);
+          if (gy) st_d2_cs(dst + (int64_t)gy * pstride_y, wn);
+          if (gx && gy) st_d2_cs(dst + (int64_t)gx * a.ldv + (int64_t)gy * pstride_y, wn);
+          if (MODE == SDB_CHEB_DOUBLING) {
+            accA.x += wn.x * wn.x;
+            accA.y += wn.y * wn.y;
+            accB.x += wn.x * xi.x;
+            accB.y += wn.y * xi.y;
+          } else {
+            const double2 p0 = FIRST ? xi : *reinterpret_cast<const double2*>(ps + SL::V0 + io[k]);
+            accA.x += p0.x * wn.x;
+            accA.y += p0.y * wn.y;
+          }
+          if (FIRST) {
+            accZ.x += xi.x * xi.x;
+            accZ.y += xi.y * xi.y;
+          }
+        }
+      }
+      if (sprev >= 0) {  // plane p-1 fully consumed
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + sprev);
+      }
+      sprev = s;
+      if (++s == t.R) {
+        s = 0;
+        phase ^= 1u;
+      }
+      pn += pplane;
+#pragma unroll
+      for (int k = 0; k < PPT; ++k) {
+        accP[k] = accC[k];
+        accC[k] = accN[k];
+        accN[k] = make_double2(0.0, 0.0);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + sprev);  // the trailing halo plane
+  }
+
+  // ---- block partials: threads with equal q hold the same columns; add them
+  // in group order through shared memory (consumers only; fixed order) ----
+  asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
+  double* red = zsm;  // every slot has been consumed: reuse the ring
+  auto partial = [&](double2 v, int slot) {
+    red[tid * 2] = v.x;
+    red[tid * 2 + 1] = v.y;
+    asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
+    if (tid < CS && pb_row >= 0) {
+      const int qq = tid / 2, comp = tid % 2;
+      double sum = 0.0;
+      for (int gg = 0; gg < GROUPS; ++gg) sum += red[(gg * L + qq) * 2 + comp];
+      a.partials[((int64_t)slot * a.nblocks + pb_row) * a.ldv + col0 + tid] = sum;
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NT) : "memory");
+  };
+  if (a.slotA >= 0) partial(accA, a.slotA);
+  if (MODE == SDB_CHEB_DOUBLING && a.slotB >= 0) partial(accB, a.slotB);
+  if (FIRST && a.slot0 >= 0) partial(accZ, a.slot0);
+}
+
+// Probe block (n x ldv) -> ghost-padded block [nz][ny+2][nx+2][ldv].
+__global__ void zm_pad_kernel(const double* __restrict__ src, int nx, int ny, int nz, int64_t ldv,
+                              double* __restrict__ dst) {
+  const int64_t pts = (int64_t)nz * (ny + 2) * (nx + 2);
+  const int64_t h = ldv / 2;  // double2 per point
+  const int64_t total = pts * h;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % h, pt = i / h;
+    const int xx = (int)(pt % (nx + 2));
+    const int64_t r = pt / (nx + 2);
+    const int yy = (int)(r % (ny + 2));
+    const int z = (int)(r / (ny + 2));
+    int x = xx - 1, y = yy - 1;
+    x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
+    y = y < 0 ? y + ny : (y >= ny ? y - ny : y);
+    const int64_t s = (((int64_t)z * ny + y) * nx + x) * ldv + 2 * c;
+    reinterpret_cast<double2*>(dst)[i] = *reinterpret_cast<const double2*>(src + s);
+  }
+}
+
+// ---- host side ---------------------------------------------------------------------
+// Tile configurations (CS probe columns, TX x TY points, PPT columns per thread);
+// 256 consumer threads (2 columns each) + 1 producer warp: 9 warps leave up
+// to 168 registers per thread.
+// zm_plan picks the first that fits; SDB_ZM_CFG overrides it (tuning).
+struct ZmCfg {
+  int CS, TX, TY, PPT;
+};
+static constexpr ZmCfg kZmCfgs[] = {
+    {8, 16, 8, 2},   // 0: 11.5 KB boxes, halo 1.41x
+    {4, 32, 8, 2},   // 1: 10.9 KB, 1.33x
+    {8, 32, 4, 2},   // 2: 13.1 KB, 1.59x
+    {16, 8, 8, 2},   // 3: 12.8 KB, 1.56x
+    {4, 16, 16, 2},  // 4: 10.4 KB, 1.27x
+    {8, 8, 8, 2},    // 5: 128 consumer threads (small grids)
+    {16, 8, 8, 1},   // 6: 512 consumer threads, one column each
+};
+constexpr int kZmNumCfgs = (int)(sizeof(kZmCfgs) / sizeof(kZmCfgs[0]));
+
+static int zm_env(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v ? atoi(v) : dflt;
+}
+
+template <int SHAPE, int CFG, int MODE, bool FIRST>
+static const void* zm_kernel() {
+  constexpr ZmCfg c = kZmCfgs[CFG];
+  return (const void*)cheb_step_zmarch<SHAPE, c.CS, c.TX, c.TY, c.PPT, MODE, FIRST>;
+}
+
+template <int SHAPE, int CFG>
+static const void* zm_kernel_rt(int mode, bool first) {
+  if (mode == SDB_CHEB_DOUBLING)
+    return first ? zm_kernel<SHAPE, CFG, SDB_CHEB_DOUBLING, true>() : zm_kernel<SHAPE, CFG, SDB_CHEB_DOUBLING, false>();
+  return first ? zm_kernel<SHAPE, CFG, SDB_CHEB_DIRECT, true>() : zm_kernel<SHAPE, CFG, SDB_CHEB_DIRECT, false>();
+}
+
+static const void* zm_kernel_for(int shape, int cfg, int mode, bool first) {
+#define SDB_ZM_CFG_CASE(C)                                                                      \
+  case C:                                                                                       \
+    return shape == SDB_SHAPE_FACE7 ? zm_kernel_rt<SDB_SHAPE_FACE7, C>(mode, first)             \
+                                    : zm_kernel_rt<SDB_SHAPE_BOX27, C>(mode, first);
+  switch (cfg) {
+    SDB_ZM_CFG_CASE(0)
+    SDB_ZM_CFG_CASE(1)
+    SDB_ZM_CFG_CASE(2)
+    SDB_ZM_CFG_CASE(3)
+    SDB_ZM_CFG_CASE(4)
+    SDB_ZM_CFG_CASE(5)
+    SDB_ZM_CFG_CASE(6)
+  }
+#undef SDB_ZM_CFG_CASE
+  return nullptr;
+}
+
+// Host mirror of ZmSlot<...>::DOUBLES.
+static int64_t zm_slot_doubles(const ZmCfg& c, int mode, bool first) {
+  auto al = [](int64_t v) { return (v + 15) / 16 * 16; };
+  const int64_t xb = (int64_t)(c.TY + 2) * (c.TX + 2) * c.CS, ib = (int64_t)c.TY * c.TX * c.CS;
+  return al(xb) + (first ? 0 : al(ib)) + ((mode == SDB_CHEB_DIRECT && !first) ? al(ib) : 0) + al((int64_t)c.TY * c.TX);
+}
+
+static bool zm_fits(const ZmCfg& c, int nx, int ny, int64_t ldv) {
+  return ldv % c.CS == 0 && nx % c.TX == 0 && ny % c.TY == 0;
+}
+
+int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* out) {
+  ZmPlan p;
+  *out = p;
+  if (m->format != SDB_FMT_STENCIL || m->zghost) return SDB_OK;
+  if (m->shape != SDB_SHAPE_FACE7 && m->shape != SDB_SHAPE_BOX27) return SDB_OK;
+  if (mode != SDB_CHEB_DIRECT && mode != SDB_CHEB_DOUBLING) return SDB_OK;
+  if (!zm_env("SDB_ZMARCH", 1)) return SDB_OK;
+  const int nx = (int)m->st.nx, ny = (int)m->st.ny, nz = (int)m->st.nz;
+  if (nx < 3 || ny < 3 || nz < 3) return SDB_OK;
+  int cfg = -1;
+  const int forced = zm_env("SDB_ZM_CFG", -1);
+  if (forced >= 0 && forced < kZmNumCfgs) {
+    if (zm_fits(kZmCfgs[forced], nx, ny, ldv)) cfg = forced;
+  } else {
+    // measured preference (profiles/r01_zmarch_sweep.txt): 16-column slices of
+    // 8x8 tiles, then 8-column slices, then the narrow / small-grid shapes
+    static const int pref[] = {3, 0, 2, 1, 4, 5};
+    for (int i = 0; i < (int)(sizeof(pref) / sizeof(pref[0])) && cfg < 0; ++i)
+      if (zm_fits(kZmCfgs[pref[i]], nx, ny, ldv)) cfg = pref[i];
+  }
+  if (cfg < 0) return SDB_OK;
+  const ZmCfg c = kZmCfgs[cfg];
+  p.cfg = cfg;
+  p.CS = c.CS;
+  p.TX = c.TX;
+  p.TY = c.TY;
+  const int slices = (int)(ldv / c.CS);
+  // ring depth from the largest slot (direct mode after the first step)
+  const int64_t slot_max = zm_slot_doubles(c, SDB_CHEB_DIRECT, false);
+  const size_t budget = 220 * 1024;
+  int R = (int)((budget - 256) / (slot_max * sizeof(double)));
+  const int rmax = zm_env("SDB_ZM_R", 8);
+  if (R > rmax) R = rmax;
+  if (R < 3) return SDB_OK;  // plane p and p-1 are held while p+1 streams in
+  p.R = R;
+  const int nt = c.TX * c.TY * (c.CS / 2) / c.PPT;
+  p.smem = (size_t)R * slot_max * sizeof(double) + 2 * R * sizeof(uint64_t);
+  if (p.smem < (size_t)nt * 2 * sizeof(double) + 2 * R * sizeof(uint64_t))
+    p.smem = (size_t)nt * 2 * sizeof(double) + 2 * R * sizeof(uint64_t);
+  // z segments: enough items to balance the persistent blocks, >= 4 planes per
+  // segment (halo planes cost (ZS+2)/ZS in L2 traffic)
+  const int sms = num_sms(m->device);
+  const int64_t base = (int64_t)(nx / c.TX) * (ny / c.TY) * slices;
+  int nzs = zm_env("SDB_ZM_NZS", 0);
+  if (nzs <= 0) {
+    nzs = (int)((4LL * sms + base - 1) / base);
+    if (nzs > nz / 4) nzs = nz / 4 > 0 ? nz / 4 : 1;
+  }
+  p.ZS = (nz + nzs - 1) / nzs;
+  p.n_zs = (nz + p.ZS - 1) / p.ZS;
+  p.items = base * p.n_zs;
+  // persistent grid: a multiple of the slice count, at most one block per SM,
+  // the largest one that minimises the busiest block's item count
+  int64_t best_g = slices, best_cost = -1;
+  for (int64_t g = (sms / slices) * slices; g >= slices; g -= slices) {
+    if (g > p.items) continue;
+    const int64_t per = (p.items + g - 1) / g;
+    if (best_cost < 0 || per < best_cost) {
+      best_cost = per;
+      best_g = g;
+    }
+  }
+  const int eg = zm_env("SDB_ZM_GRID", 0);
+  if (eg > 0) best_g = (eg / slices) * slices > 0 ? (eg / slices) * slices : slices;
+  if (best_g > p.items) best_g = p.items;
+  p.grid = best_g;
+  p.nbp = p.grid / slices;
+  p.block_bytes = sizeof(double) * (size_t)nz * (ny + 2) * (nx + 2) * (size_t)ldv;
+  p.block_bytes = (p.block_bytes + 255) & ~(size_t)255;
+  p.name = "cheb_step_zmarch";
+  p.on = true;
+  *out = p;
+  return SDB_OK;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+  static std::once_flag once;
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+  });
+  return fn;
+}
+
+int zm_launch_step(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, bool first, int mode, cudaStream_t s) {
+  auto enc = tensor_map_encoder();
+  if (!enc) return fail(SDB_ECUDA, "cuTensorMapEncodeTiled is not available from the driver");
+  const int nx = (int)m->st.nx, ny = (int)m->st.ny, nz = (int)m->st.nz;
+  const ZmCfg c = kZmCfgs[p.cfg];
+  ZmMaps maps;
+  auto encode = [&](CUtensorMap* map, const double* base, int bx, int by) -> int {
+    cuuint64_t gdim[4] = {(cuuint64_t)a.ldv, (cuuint64_t)(nx + 2), (cuuint64_t)(ny + 2), (cuuint64_t)nz};
+    cuuint64_t gstr[3] = {(cuuint64_t)a.ldv * 8, (cuuint64_t)(nx + 2) * a.ldv * 8,
+                          (cuuint64_t)(ny + 2) * (nx + 2) * a.ldv * 8};
+    cuuint32_t box[4] = {(cuuint32_t)c.CS, (cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(base), gdim, gstr, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? SDB_OK : fail(SDB_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  };
+  int rc;
+  if ((rc = encode(&maps.x, a.x, c.TX + 2, c.TY + 2))) return rc;
+  if ((rc = encode(&maps.prev, a.prev ? a.prev : a.x, c.TX, c.TY))) return rc;
+  if ((rc = encode(&maps.v0, a.v0 ? a.v0 : a.x, c.TX, c.TY))) return rc;
+  {
+    cuuint64_t gdim[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+    cuuint64_t gstr[2] = {(cuuint64_t)nx * 8, (cuuint64_t)nx * ny * 8};
+    cuuint32_t box[3] = {(cuuint32_t)c.TX, (cuuint32_t)c.TY, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&maps.diag, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(m->diag), gdim, gstr, box,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(SDB_ECUDA, "cuTensorMapEncodeTiled (diag) failed (%d)", (int)r);
+  }
+  ZmArgs t{};
+  t.nx = nx;
+  t.ny = ny;
+  t.nz = nz;
+  t.n_xt = nx / c.TX;
+  t.n_yt = ny / c.TY;
+  t.n_zs = p.n_zs;
+  t.ZS = p.ZS;
+  t.slices = (int)(a.ldv / c.CS);
+  t.R = p.R;
+  t.items = p.items;
+  t.diag = m->diag;
+  for (int o = 0; o < 27; ++o) t.wc[o] = o < m->nterms ? m->term_w_host[o] : 0.0;
+  StepArgs aa = a;
+  aa.nblocks = p.nbp;
+  const void* fn = zm_kernel_for(m->shape, p.cfg, mode, first);
+  if (!fn) return fail(SDB_EUNSUPPORTED, "no z-march kernel for configuration %d", p.cfg);
+  size_t smem = (size_t)p.R * zm_slot_doubles(c, mode, first) * sizeof(double) + 2 * p.R * sizeof(uint64_t);
+  const int nt = c.TX * c.TY * (c.CS / 2) / c.PPT;
+  if (smem < (size_t)nt * 2 * sizeof(double) + 2 * p.R * sizeof(uint64_t))
+    smem = (size_t)nt * 2 * sizeof(double) + 2 * p.R * sizeof(uint64_t);
+  SDB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  void* args[] = {(void*)&maps, (void*)&t, (void*)&aa};
+  SDB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)p.grid), dim3(nt + 32), args, smem, s));
+  return SDB_OK;
+}
+
+int zm_pad(const sdb_matrix* m, const double* probes, int64_t ldv, double* padded, cudaStream_t s) {
+  const int nx = (int)m->st.nx, ny = (int)m->st.ny, nz = (int)m->st.nz;
+  const int64_t total = (int64_t)nz * (ny + 2) * (nx + 2) * (ldv / 2);
+  int64_t blocks = (total + 255) / 256;
+  const int64_t cap = 8LL * num_sms(m->device);
+  if (blocks > cap) blocks = cap;
+  zm_pad_kernel<<<(unsigned)blocks, 256, 0, s>>>(probes, nx, ny, nz, ldv, padded);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+}  // namespace sdb
