@@ -61,6 +61,8 @@ extern "C" {
 #define SDB_CHEB_DIRECT 0   /* zeta_k = v0 . w_k, degree matvecs / probe (kpm.py:96-107)     */
 #define SDB_CHEB_DOUBLING 1 /* zeta_{2k}=2<w_k,w_k>-zeta_0, zeta_{2k+1}=2<w_{k+1},w_k>-zeta_1;
                                (degree+1)/2 matvecs / probe (kpm.py:157-198)                  */
+#define SDB_LEGENDRE 2      /* zeta_k = v0 . L_k(B) v0, (k+1)L_{k+1} = (2k+1)B L_k - k L_{k-1}
+                             (kpm.py:110-124, :150-154); direct-mode kernels                    */
 
 /* damping kinds (kpm.py:62-93) */
 #define SDB_DAMP_NONE 0
@@ -189,6 +191,10 @@ SDB_API int sdb_kpm_coefficients(const double* zeta, int64_t degree, int64_t n, 
 SDB_API int sdb_chebyshev_series(const double* mu, int64_t degree, const double* t, int64_t n_pts,
                          int edge_weight, double divisor, double* values, double* density,
                          void* stream);
+/* values[i] = sum_k c_k L_k(t_i) (Legendre forward recurrence, kpm.py:220-231);
+ * density[i] = values[i] / divisor (density may be NULL).  Device pointers. */
+SDB_API int sdb_legendre_series(const double* c, int64_t degree, const double* t, int64_t n_pts,
+                        double divisor, double* values, double* density, void* stream);
 
 /* ---- Lanczos quadrature (lanczos.py:67-219) ----------------------------- */
 SDB_API int sdb_lanczos_workspace_size(const sdb_matrix* m, int64_t n_vec, int64_t steps,

@@ -115,6 +115,21 @@ def doubling_probe_moments(csr, c, d, degree, v0):
     return zeta
 
 
+# ---- kpm.py:110-124 (Legendre recurrence, one probe) -----------------------------------------
+def legendre_probe_moments(csr, c, d, degree, v0):
+    zeta = np.empty(degree + 1)
+    zeta[0] = v0 @ v0
+    if degree == 0:
+        return zeta
+    v_prev = v0
+    v_cur = mapped_matvec(csr, c, d, v0)
+    zeta[1] = v0 @ v_cur
+    for k in range(1, degree):
+        v_cur, v_prev = ((2 * k + 1) * mapped_matvec(csr, c, d, v_cur) - k * v_prev) / (k + 1.0), v_cur
+        zeta[k + 1] = v0 @ v_cur
+    return zeta
+
+
 # ---- kpm.py:127-140 ----------------------------------------------------------------------
 def average_moments(per_probe):
     zeta = np.mean(np.asarray(per_probe), axis=0)
@@ -128,7 +143,7 @@ def chebyshev_moments(matrix, c, d, degree, kind, seed, n_vec, mode="direct", st
     csr = as_csr(matrix)
     n = csr.shape[0]
     fn = {"direct": chebyshev_probe_moments, "product": product_formula_probe_moments,
-          "doubling": doubling_probe_moments}[mode]
+          "doubling": doubling_probe_moments, "legendre": legendre_probe_moments}[mode]
     idx = range(n_vec) if indices is None else indices
     return np.array([fn(csr, c, d, degree, draw_probe(kind, seed, n, l, stream)) for l in idx])
 
@@ -173,6 +188,47 @@ def evaluate_kpm_dos(coeffs, d, t):
     if np.any(np.abs(t) > 1.0 - EDGE_GUARD):
         raise ValueError("grid point too close to the interval edge")
     values = evaluate_chebyshev_series(coeffs, t) / np.sqrt(1.0 - t * t)
+    return values, values / d
+
+
+# ---- kpm.py:220-231, :253-308 (moment-sharing variants) -------------------------------------
+def evaluate_legendre_series(coeffs, t):
+    acc = coeffs[0] * np.ones_like(t)
+    if len(coeffs) == 1:
+        return acc
+    l_prev = np.ones_like(t)
+    l_cur = np.asarray(t, dtype=float)
+    acc = acc + coeffs[1] * l_cur
+    for k in range(1, len(coeffs) - 1):
+        l_cur, l_prev = ((2 * k + 1) * t * l_cur - k * l_prev) / (k + 1.0), l_cur
+        acc += coeffs[k + 1] * l_cur
+    return acc
+
+
+def kpml_dos(zeta, n, d, t):
+    """(values, density): sum_k (k + 1/2) zeta_k/n L_k(t), unmapped by 1/d (kpm.py:298-308)."""
+    k = np.arange(len(zeta))
+    values = evaluate_legendre_series((k + 0.5) * zeta / n, t)
+    return values, values / d
+
+
+def spectroscopic_dos(zeta, n, d, t):
+    """Undamped KPM with the top coefficient halved (kpm.py:253-266)."""
+    coeffs = moments_to_coefficients(zeta, n, "none")
+    if len(zeta) >= 2:
+        coeffs = coeffs.copy()
+        coeffs[-1] *= 0.5
+    return evaluate_kpm_dos(coeffs, d, t)
+
+
+def delta_chebyshev_dos(zeta, n, d, t, degrees):
+    """Per-point truncation degrees of the undamped series (kpm.py:269-295)."""
+    coeffs = moments_to_coefficients(zeta, n, "none")
+    values = np.empty_like(t)
+    for deg in np.unique(degrees):
+        mask = degrees == deg
+        ts = t[mask]
+        values[mask] = evaluate_chebyshev_series(coeffs[: deg + 1], ts) / np.sqrt(1.0 - ts * ts)
     return values, values / d
 
 

@@ -4,9 +4,11 @@ Methods on the hot path: ``kpm``, ``kpm-jackson`` (direct or product-formula
 moments) and ``lanczos``.  For the KPM methods the whole chain -- moments,
 probe mean, finiteness check, coefficients, Clenshaw, 1/sqrt(1-t^2) and the
 1/d unmapping -- stays on the device and the host reads back the moments and
-the density once.  The other reference methods (spectroscopic, delta-cheb,
-kpml, dgl, haydock, cdos) are outside the accelerated path and
-raise ``NotImplementedError``.
+the density once.  The moment-sharing variants ``spectroscopic``,
+``delta-cheb`` (same Chebyshev moments) and ``kpml`` (Legendre moments from
+the same fused kernels) run through the same kernels.  The
+remaining reference methods (dgl, haydock, cdos) are outside the accelerated
+path and raise ``NotImplementedError``.
 """
 
 import time
@@ -15,6 +17,7 @@ import numpy as np
 
 from . import _native
 from . import engine as E
+from . import kpm as K
 from .density import DEFAULT_GRID_POINTS, SpectralDensityEstimate, interval_grid, unit_grid
 from .errors import NumericalFailure
 from .lanczos import lanczos_dos
@@ -24,7 +27,7 @@ CHEBYSHEV_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb")
 LEGENDRE_METHODS = ("kpml", "dgl")
 LANCZOS_METHODS = ("lanczos", "haydock", "cdos")
 ALL_METHODS = CHEBYSHEV_METHODS + LEGENDRE_METHODS + LANCZOS_METHODS
-GPU_METHODS = ("kpm", "kpm-jackson", "lanczos")
+GPU_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb", "kpml", "lanczos")
 
 
 def analytic_matvec_count(method, degree, n_vec, product_formula=False):
@@ -91,6 +94,19 @@ def estimate_dos(matrix, interval, method, degree, source, n_vec, sigma=None, et
             est.method = "kpm-jackson"
             est.params["damping"] = "jackson"
         est.params["moments"] = zeta
+    elif method in ("spectroscopic", "delta-cheb"):
+        mapped = apply_spectral_map(counter, interval)
+        compute = K.moments_via_product_formula if product_formula else K.compute_chebyshev_moments
+        moments = compute(mapped, degree, source, n_vec, threads, device=device)
+        grid = unit_grid(grid_points)
+        if method == "spectroscopic":
+            est = K.spectroscopic_dos(moments, interval, grid, device=device)
+        else:
+            est = K.delta_chebyshev_dos(moments, interval, grid, device=device)
+    elif method == "kpml":
+        mapped = apply_spectral_map(counter, interval)
+        moments = K.compute_legendre_moments(mapped, degree, source, n_vec, threads, device=device)
+        est = K.evaluate_kpml_dos(moments, interval, unit_grid(grid_points), device=device)
     else:
         grid = interval_grid(interval, grid_points)
         est = lanczos_dos(counter, interval, degree, source, n_vec, sigma, grid, threads, device=device)

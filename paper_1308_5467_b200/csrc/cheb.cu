@@ -81,6 +81,9 @@ __device__ __forceinline__ void epi_finish(const StepArgs& a, int64_t row, int q
     double2 wn;
     if (FIRST) {
       wn = make_double2(tx, ty);
+    } else if (MODE == SDB_CHEB_DIRECT && a.legendre) {
+      wn.x = (a.la * tx - a.lb * e.wp[v].x) / a.lc;
+      wn.y = (a.la * ty - a.lb * e.wp[v].y) / a.lc;
     } else {
       wn.x = 2.0 * tx - e.wp[v].x;
       wn.y = 2.0 * ty - e.wp[v].y;
@@ -701,6 +704,7 @@ static int launch_plan_step(const sdb_matrix* m, const StepPlan& P, int64_t degr
   a.prev = prev;
   a.next = next;
   a.slot0 = (k == 0) ? 0 : -1;
+  set_step_scalars(a, k);
   if (mode == SDB_CHEB_DOUBLING) {
     a.slotB = (2 * k + 1 <= degree) ? (int)(2 * k + 1) : -1;
     a.slotA = (2 * k + 2 <= degree) ? (int)(2 * k + 2) : -1;
@@ -747,6 +751,8 @@ using namespace sdb;
 extern "C" {
 
 int sdb_cheb_workspace_size(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode, size_t* bytes) {
+  int leg_;
+  mode = split_mode(mode, &leg_);
   SDB_REQUIRE(m && bytes, "NULL argument");
   SDB_REQUIRE(n_vec >= 1 && n_vec <= SDB_MAX_BATCH, "n_vec must lie in [1, %d] per batch", SDB_MAX_BATCH);
   SDB_REQUIRE(degree >= 0, "degree must be non-negative");
@@ -763,6 +769,8 @@ int sdb_cheb_workspace_size(const sdb_matrix* m, int64_t n_vec, int64_t degree, 
 }
 
 const char* sdb_cheb_kernel(const sdb_matrix* m, int64_t n_vec, int mode) {
+  int leg_;
+  mode = split_mode(mode, &leg_);
   if (!m || n_vec < 1 || n_vec > SDB_MAX_BATCH) return "";
   const Geometry g = choose_geometry(n_vec);
   ZmPlan zp;
@@ -777,6 +785,8 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
                      const double* probes, double* zeta_pp, void* workspace, size_t workspace_bytes, void* stream,
                      float* step_ms) {
   SDB_REQUIRE(m && probes && zeta_pp, "NULL argument");
+  int legendre;
+  mode = split_mode(mode, &legendre);
   size_t need = 0;
   int rc = sdb_cheb_workspace_size(m, n_vec, degree, mode, &need);
   if (rc) return rc;
@@ -788,6 +798,7 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
   cudaStream_t s = (cudaStream_t)stream;
   StepPlan P;
   if ((rc = plan_steps(m, n_vec, mode, c, d, &P))) return rc;
+  P.a.legendre = legendre;
   size_t bb, pb;
   cheb_layout(m, P.g.ldv, degree, &bb, &pb);
   ZmPlan zp;
@@ -823,6 +834,7 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
       a.prev = prev;
       a.next = next;
       a.slot0 = (k == 0) ? 0 : -1;
+      set_step_scalars(a, k);
       if (mode == SDB_CHEB_DOUBLING) {
         a.slotB = (2 * k + 1 <= degree) ? (int)(2 * k + 1) : -1;
         a.slotA = (2 * k + 2 <= degree) ? (int)(2 * k + 2) : -1;
@@ -864,6 +876,8 @@ int sdb_cheb_step(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_
                   const double* x, const double* prev, double* next, const double* v0, double* partials,
                   size_t partial_bytes, void* stream) {
   SDB_REQUIRE(m && x && partials, "NULL argument");
+  int legendre;
+  mode = split_mode(mode, &legendre);
   size_t pb = 0;
   int rc = sdb_cheb_partials_size(m, n_vec, degree, mode, &pb);
   if (rc) return rc;
@@ -879,11 +893,14 @@ int sdb_cheb_step(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_
   if (!dg.ok) return fail(SDB_ECUDA, "cannot select CUDA device %d", m->device);
   StepPlan P;
   if ((rc = plan_steps(m, n_vec, mode, c, d, &P))) return rc;
+  P.a.legendre = legendre;
   return launch_plan_step(m, P, degree, mode, k, x, prev, next, v0 ? v0 : x, partials, (cudaStream_t)stream);
 }
 
 int sdb_cheb_reduce(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode, const double* partials,
                     double* zeta_pp, void* stream) {
+  int leg_;
+  mode = split_mode(mode, &leg_);
   SDB_REQUIRE(m && partials && zeta_pp, "NULL argument");
   SDB_REQUIRE(n_vec >= 1 && n_vec <= SDB_MAX_BATCH && degree >= 0, "bad shape");
   DeviceGuard dg(m->device);

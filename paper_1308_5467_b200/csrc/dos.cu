@@ -72,6 +72,39 @@ __global__ void series_kernel(const double* __restrict__ mu, int64_t degree, con
   if (density) density[i] = v / divisor;
 }
 
+// KPML evaluation (kpm.py:220-231, :298-308): sum_k c_k L_k(t) by the forward
+// recurrence L_{k+1} = ((2k+1) t L_k - k L_{k-1}) / (k+1), one grid point per
+// thread, in the reference's expression order; density = values / divisor.
+__global__ void legendre_series_kernel(const double* __restrict__ c, int64_t degree, const double* __restrict__ t,
+                                       int64_t n_pts, double divisor, double* __restrict__ values,
+                                       double* __restrict__ density) {
+  constexpr int TILE = 1024;
+  __shared__ double cs[TILE];
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool live = i < n_pts;
+  const double ti = live ? t[i] : 0.0;
+  double acc = c[0] * 1.0;
+  double lp = 1.0, lc = ti;
+  if (degree >= 1) acc = acc + c[1] * lc;
+  // coefficients 2..M in tiles; step k produces L_{k+1}
+  for (int64_t lo = 2; lo <= degree; lo += TILE) {
+    const int64_t hi = lo + TILE - 1 < degree ? lo + TILE - 1 : degree;
+    __syncthreads();
+    for (int64_t k = lo + threadIdx.x; k <= hi; k += blockDim.x) cs[k - lo] = c[k];
+    __syncthreads();
+    for (int64_t k1 = lo; k1 <= hi; ++k1) {
+      const int64_t k = k1 - 1;
+      const double ln = ((double)(2 * k + 1) * ti * lc - (double)k * lp) / ((double)k + 1.0);
+      lp = lc;
+      lc = ln;
+      acc += cs[k1 - lo] * lc;
+    }
+  }
+  if (!live) return;
+  values[i] = acc;
+  if (density) density[i] = acc / divisor;
+}
+
 // ---- K6: batched first-row implicit QL ---------------------------------------------
 // ritz_quadrature (lanczos.py:152-159) takes theta, y = eigh_tridiagonal(alpha,
 // beta) and tau^2 = y[0,:]^2.  Only the first row of the eigenvector matrix is
@@ -275,6 +308,18 @@ int sdb_chebyshev_series(const double* mu, int64_t degree, const double* t, int6
   int blocks = (int)((n_pts + 127) / 128);
   series_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(mu, degree, t, n_pts, edge_weight, divisor, values,
                                                           density);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+int sdb_legendre_series(const double* c, int64_t degree, const double* t, int64_t n_pts, double divisor,
+                        double* values, double* density, void* stream) {
+  SDB_REQUIRE(c && t && values, "NULL argument");
+  SDB_REQUIRE(degree >= 0, "degree must be non-negative");
+  if (n_pts <= 0) return SDB_OK;
+  SDB_REQUIRE(density == nullptr || divisor != 0.0, "divisor must be non-zero");
+  int blocks = (int)((n_pts + 127) / 128);
+  legendre_series_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(c, degree, t, n_pts, divisor, values, density);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

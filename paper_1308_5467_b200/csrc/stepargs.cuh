@@ -21,7 +21,22 @@ struct StepArgs {
   int slotB;           // doubling: <w+,w>                       (-1: none)
   int slot0;           // step 0: <w0,w0>                        (-1: none)
   int slices;          // column slices per panel (grid kernel; 1 = whole rows)
+  // Legendre recurrence (kpm.py:110-124), direct-mode kernels after step 0:
+  // w_{k+1} = (la t - lb w_{k-1}) / lc with la = 2k+1, lb = k, lc = k+1
+  int legendre;
+  double la, lb, lc;
 };
+
+// SDB_LEGENDRE runs the direct-mode kernels with the Legendre update.
+inline int split_mode(int mode, int* legendre) {
+  *legendre = mode == SDB_LEGENDRE;
+  return mode == SDB_LEGENDRE ? SDB_CHEB_DIRECT : mode;
+}
+inline void set_step_scalars(StepArgs& a, int64_t k) {
+  a.la = (double)(2 * k + 1);
+  a.lb = (double)k;
+  a.lc = (double)k + 1.0;
+}
 
 // Structured-grid term order (7-point faces, 27-point box): lexicographic in
 // (dz, dy, dx), which is the sorted-column order of the stencil's CSR form for

@@ -283,7 +283,10 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
             wn = make_double2(tx, ty);
           } else {
             const double2 wp = *reinterpret_cast<const double2*>(ps + SL::P0 + io[k]);
-            wn = make_double2(2.0 * tx - wp.x, 2.0 * ty - wp.y);
+            if (MODE == SDB_CHEB_DIRECT && a.legendre)
+              wn = make_double2((a.la * tx - a.lb * wp.x) / a.lc, (a.la * ty - a.lb * wp.y) / a.lc);
+            else
+              wn = make_double2(2.0 * tx - wp.x, 2.0 * ty - wp.y);
           }
           double* dst = pn + cofs[k];
           st_d2_cs(dst, wn);
@@ -439,6 +442,8 @@ static bool zm_fits(const ZmCfg& c, int nx, int ny, int64_t ldv) {
 }
 
 int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* out) {
+  int leg_;
+  mode = split_mode(mode, &leg_);
   ZmPlan p;
   *out = p;
   if (m->format != SDB_FMT_STENCIL || m->zghost) return SDB_OK;

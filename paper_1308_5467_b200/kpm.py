@@ -10,6 +10,11 @@ libspecdens_b200.so:
   moments_to_coefficients     kpm.py:201-208  -> sdb_kpm_coefficients
   evaluate_chebyshev_series   kpm.py:211-217  -> sdb_chebyshev_series
   evaluate_kpm_dos            kpm.py:244-250  -> sdb_chebyshev_series (+1/sqrt(1-t^2), /d)
+  compute_legendre_moments    kpm.py:110-124, :150-154 -> K1 direct-mode kernels, Legendre update
+  evaluate_legendre_series    kpm.py:220-231  -> sdb_legendre_series
+  evaluate_kpml_dos           kpm.py:298-308  -> sdb_legendre_series (/d)
+  spectroscopic_dos           kpm.py:253-266  -> coefficients + series kernels
+  delta_chebyshev_dos         kpm.py:269-295  -> series kernel per truncation degree
 
 ``threads`` is accepted for signature compatibility and ignored: the probes
 already run concurrently on the device and results are deterministic.
@@ -85,7 +90,8 @@ def _moments(op, degree, source, n_vec, mode, device=None):
     E.credit_counters(run.resolved, n_vec, run.matvecs_per_probe)
     if int(flag.item()) != 0 or not np.all(np.isfinite(zeta)):
         raise NumericalFailure(SPECTRUM_ESCAPE_HINT)
-    return MomentSequence(zeta=zeta, degree=degree, n_vec=n_vec, basis="chebyshev", n=run.n)
+    basis = "legendre" if mode == _native.SDB_LEGENDRE else "chebyshev"
+    return MomentSequence(zeta=zeta, degree=degree, n_vec=n_vec, basis=basis, n=run.n)
 
 
 def compute_chebyshev_moments(op, degree, source, n_vec, threads=None, device=None):
@@ -95,6 +101,15 @@ def compute_chebyshev_moments(op, degree, source, n_vec, threads=None, device=No
     if degree < 0:
         raise ValueError("degree must be non-negative")
     return _moments(op, degree, source, n_vec, _native.SDB_CHEB_DIRECT, device)
+
+
+def compute_legendre_moments(op, degree, source, n_vec, threads=None, device=None):
+    """Legendre moments via (k+1)L_{k+1} = (2k+1)tL_k - kL_{k-1} (kpm.py:110-124, :150-154)."""
+    if n_vec < 1:
+        raise ValueError("need at least one probe vector")
+    if degree < 0:
+        raise ValueError("degree must be non-negative")
+    return _moments(op, degree, source, n_vec, _native.SDB_LEGENDRE, device)
 
 
 def moments_via_product_formula(op, degree, source, n_vec, threads=None, max_stored_vectors=None, device=None):
@@ -183,3 +198,88 @@ def evaluate_kpm_dos(coeffs, interval, grid=None, device=None):
     return SpectralDensityEstimate.from_parts(
         t, v, interval.from_unit(t), den, interval, method="kpm", params={"degree": len(coeffs) - 1}
     )
+
+
+def evaluate_legendre_series(coeffs, t, device=None):
+    """Forward-recurrence evaluation of sum_k coeffs[k] L_k(t) (kpm.py:220-231)."""
+    coeffs = np.asarray(coeffs, dtype=float)
+    t_arr = np.asarray(t, dtype=float)
+    torch = E._torch()
+    device = E.require_cuda(device)
+    with torch.cuda.device(device):
+        c = E.to_device(coeffs, device)
+        tt = E.to_device(t_arr.ravel(), device)
+        out = torch.empty_like(tt)
+        _native.call("sdb_legendre_series", E.ptr(c), len(coeffs) - 1, E.ptr(tt), tt.numel(), 1.0, E.ptr(out), None,
+                     E.stream_ptr(device))
+        return out.cpu().numpy().reshape(t_arr.shape)
+
+
+def evaluate_kpml_dos(moments, interval, grid=None, device=None):
+    """Legendre-basis density sum_k (k + 1/2) zeta_k/n L_k(t), no edge weight (kpm.py:298-308)."""
+    if moments.basis != "legendre":
+        raise ValueError("KPML evaluation needs legendre moments")
+    t = _checked_unit_points(grid)
+    k = np.arange(moments.degree + 1)
+    coeffs = (k + 0.5) * moments.zeta / moments.n
+    torch = E._torch()
+    device = E.require_cuda(device)
+    d = float(interval.halfwidth)
+    with torch.cuda.device(device):
+        c = E.to_device(coeffs, device)
+        tt = E.to_device(t, device)
+        values = torch.empty_like(tt)
+        density = torch.empty_like(tt)
+        _native.call("sdb_legendre_series", E.ptr(c), int(moments.degree), E.ptr(tt), tt.numel(), d, E.ptr(values),
+                     E.ptr(density), E.stream_ptr(device))
+        v = values.cpu().numpy()
+        den = density.cpu().numpy()
+    return SpectralDensityEstimate.from_parts(t, v, interval.from_unit(t), den, interval, method="kpml",
+                                              params={"degree": moments.degree})
+
+
+def spectroscopic_dos(moments, interval, grid=None, device=None):
+    """Undamped KPM with the top coefficient halved (kpm.py:253-266)."""
+    coeffs = moments_to_coefficients(moments, damping="none", device=device)
+    if moments.degree >= 1:
+        coeffs = coeffs.copy()
+        coeffs[-1] *= 0.5
+    est = evaluate_kpm_dos(coeffs, interval, grid=grid, device=device)
+    est.method = "spectroscopic"
+    return est
+
+
+def delta_chebyshev_dos(moments, interval, grid=None, degrees=None, device=None):
+    """Per-point-degree truncations of the undamped Chebyshev expansion (kpm.py:269-295).
+
+    Points sharing a truncation degree go through the same Clenshaw kernel as
+    KPM, so the uniform case is bit-identical to undamped KPM.
+    """
+    t = _checked_unit_points(grid)
+    if degrees is None:
+        degrees = np.full(len(t), moments.degree, dtype=int)
+    degrees = np.asarray(degrees, dtype=int)
+    if degrees.shape != t.shape:
+        raise ValueError("degrees must match the grid point for point")
+    if np.any(degrees < 0) or np.any(degrees > moments.degree):
+        raise ValueError(f"per-point degrees must lie in [0, {moments.degree}]")
+    coeffs = moments_to_coefficients(moments, damping="none", device=device)
+    torch = E._torch()
+    device = E.require_cuda(device)
+    d = float(interval.halfwidth)
+    values = np.empty_like(t)
+    density = np.empty_like(t)
+    with torch.cuda.device(device):
+        c = E.to_device(coeffs, device)
+        for deg in np.unique(degrees):
+            mask = degrees == deg
+            tt = E.to_device(t[mask], device)
+            v = torch.empty_like(tt)
+            den = torch.empty_like(tt)
+            _native.call("sdb_chebyshev_series", E.ptr(c), int(deg), E.ptr(tt), tt.numel(), 1, d, E.ptr(v),
+                         E.ptr(den), E.stream_ptr(device))
+            values[mask] = v.cpu().numpy()
+            density[mask] = den.cpu().numpy()
+    return SpectralDensityEstimate.from_parts(t, values, interval.from_unit(t), density, interval,
+                                              method="delta-cheb",
+                                              params={"degree": moments.degree, "degrees": degrees})

@@ -30,7 +30,11 @@ from specdens import (  # noqa: E402
     SparseSymmetricMatrix,
     apply_spectral_map,
     compute_chebyshev_moments,
+    compute_legendre_moments,
+    delta_chebyshev_dos,
     estimate_dos,
+    evaluate_kpml_dos,
+    spectroscopic_dos,
     evaluate_kpm_dos,
     lanczos_dos,
     lanczos_factorize,
@@ -118,6 +122,34 @@ def lanczos_case(name, op, kind, n_vec, steps, sigma, n_pts):
     )
 
 
+def variants_case(name, op, kind, n_vec, degree, n_pts):
+    """Moment-sharing variants: Legendre moments + KPML, spectroscopic, delta-Chebyshev."""
+    t0 = time.time()
+    mat = ref_matrix(op)
+    g = W.gershgorin_interval(op)
+    iv = SpectralInterval(g.lambda_lb, g.lambda_ub)
+    src = ProbeVectorSource(kind, seed=0, dim=mat.dim)
+    mapped = apply_spectral_map(mat, iv)
+    grid = unit_grid(n_pts)
+    leg = compute_legendre_moments(mapped, degree, src, n_vec)
+    kpml = evaluate_kpml_dos(leg, iv, grid)
+    cheb = compute_chebyshev_moments(mapped, degree, src, n_vec)
+    spec = spectroscopic_dos(cheb, iv, grid)
+    rng = np.random.default_rng(7)
+    degrees = rng.integers(0, degree + 1, n_pts)
+    delta = delta_chebyshev_dos(cheb, iv, grid, degrees=degrees)
+    out = dict(kind=kind, n_vec=n_vec, degree=degree, n_pts=n_pts, lb=iv.lambda_lb, ub=iv.lambda_ub,
+               zeta_legendre=leg.zeta, kpml_values=kpml.values, kpml_density=kpml.density,
+               zeta_chebyshev=cheb.zeta, spectroscopic_density=spec.density, delta_degrees=degrees,
+               delta_density=delta.density, matrix_sha256=csr_digest(mat.csr), n=mat.dim)
+    for method in ("kpml", "spectroscopic", "delta-cheb"):
+        est = estimate_dos(mat, iv, method, degree, src, n_vec, grid_points=n_pts)
+        out[f"estimate_{method}_density"] = est.density
+        out[f"estimate_{method}_matvec_count"] = est.params["matvec_count"]
+    print(f"{name}: n={mat.dim} {time.time() - t0:.1f}s", flush=True)
+    return out
+
+
 def main():
     meta = dict(numpy=np.__version__, scipy=scipy.__version__, specdens=specdens.__version__,
                 python=sys.version.split()[0])
@@ -128,6 +160,9 @@ def main():
         "c5_small": lambda: kpm_case("c5_small", W.stencil27_3d(24), "rademacher", 2, 200, 2000),
         "c4_subset": lambda: lanczos_case("c4_subset", W.build_matrix("C4"), "gaussian", 4, 100, 0.01, 2000),
         "lanczos_small": lambda: lanczos_case("lanczos_small", W.anderson_3d(8), "gaussian", 6, 40, 0.05, 400),
+        "variants_c1": lambda: variants_case("variants_c1", W.build_matrix("C1"), "gaussian", 20, 100, 1000),
+        "variants_c5small": lambda: variants_case("variants_c5small", W.stencil27_3d(24), "rademacher", 32, 60,
+                                                  500),
     }
     only = sys.argv[1:]
     for name, fn in cases.items():

@@ -91,3 +91,27 @@ def test_oracle_small_contracts():
         O.evaluate_kpm_dos(np.array([1.0]), 1.0, np.array([1.0]))
     with pytest.raises(O.OracleNumericalFailure):
         O.average_moments(O.chebyshev_moments(np.diag([3.0]), 0.0, 1.0, 800, "gaussian", 0, 1))
+
+
+VARIANT_CASES = {"variants_c1": lambda: W.build_matrix("C1"), "variants_c5small": lambda: W.stencil27_3d(24)}
+
+
+@pytest.mark.parametrize("name", list(VARIANT_CASES))
+def test_oracle_variants_match_reference(golden, name):
+    """Legendre moments, KPML, spectroscopic and delta-Chebyshev (kpm.py:110-124, :220-308)."""
+    g = golden(name)
+    op = VARIANT_CASES[name]()
+    assert csr_digest(op.csr) == str(g["matrix_sha256"])
+    lb, ub = float(g["lb"]), float(g["ub"])
+    c, d = 0.5 * (lb + ub), 0.5 * (ub - lb)
+    n_vec, degree, n = int(g["n_vec"]), int(g["degree"]), int(g["n"])
+    t = O.unit_grid(int(g["n_pts"]))
+    leg = O.average_moments(O.chebyshev_moments(op.csr, c, d, degree, str(g["kind"]), 0, n_vec, mode="legendre"))
+    np.testing.assert_array_equal(leg, g["zeta_legendre"])
+    vals, dens = O.kpml_dos(leg, n, d, t)
+    np.testing.assert_array_equal(vals, g["kpml_values"])
+    np.testing.assert_array_equal(dens, g["kpml_density"])
+    cheb = O.average_moments(O.chebyshev_moments(op.csr, c, d, degree, str(g["kind"]), 0, n_vec))
+    np.testing.assert_array_equal(cheb, g["zeta_chebyshev"])
+    np.testing.assert_array_equal(O.spectroscopic_dos(cheb, n, d, t)[1], g["spectroscopic_density"])
+    np.testing.assert_array_equal(O.delta_chebyshev_dos(cheb, n, d, t, g["delta_degrees"])[1], g["delta_density"])
