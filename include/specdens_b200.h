@@ -219,6 +219,11 @@ SDB_API int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, 
  * components.  Outputs n_vec x m; unused tail entries are set to 0. */
 SDB_API int sdb_ritz_quadrature(const double* alpha, const double* beta, const int32_t* steps_done,
                         int64_t n_vec, int64_t m, double* theta, double* tau2, void* stream);
+/* ritz_residual_bounds (lanczos.py:162-167): theta as above and
+ * resid[l][i] = |beta_next| |y[last, i]| (beta_next = beta[l][steps_done[l]-1],
+ * the sdb_lanczos layout).  Outputs n_vec x m; tails zeroed. */
+SDB_API int sdb_ritz_residual_bounds(const double* alpha, const double* beta, const int32_t* steps_done,
+                             int64_t n_vec, int64_t m, double* theta, double* resid, void* stream);
 /* pool_ritz_quadratures (lanczos.py:170-177): concatenate the first
  * steps_done[l] entries of every row l of theta/tau2 (n_rows x m), divide the
  * weights by `divisor` (the number of probes) and sort by theta (stable: ties

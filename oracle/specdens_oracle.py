@@ -330,3 +330,30 @@ def gershgorin(csr):
     dg = np.bincount(rows[on], weights=csr.data[on], minlength=n)
     rad = np.bincount(rows[~on], weights=np.abs(csr.data[~on]), minlength=n)
     return float(np.min(dg - rad)), float(np.max(dg + rad))
+
+
+# ---- lanczos.py:162-167, matrix.py:207-241 (spectral-interval estimation) -----------------------
+def ritz_residual_bounds(alpha, beta, beta_next):
+    if len(alpha) == 1:
+        return alpha.copy(), np.array([abs(beta_next)])
+    theta, y = eigh_tridiagonal(alpha, beta)
+    return theta, abs(beta_next) * np.abs(y[-1, :])
+
+
+def estimate_spectral_interval(matrix, lanczos_steps=20, margin=0.01, seed=0):
+    """(lb, ub) after widening: extreme Ritz values -/+ residual bounds (matrix.py:207-241)."""
+    csr = as_csr(matrix)
+    n = csr.shape[0]
+    steps = min(lanczos_steps, n)
+    v0 = draw_probe("gaussian", seed, n, 0, stream=0xB0)
+    if np.linalg.norm(v0) == 0.0:
+        v0 = draw_probe("gaussian", seed, n, 1, stream=0xB0)
+    alpha, beta, beta_next, _, _ = lanczos_factorize(csr, v0, steps)
+    theta, resid = ritz_residual_bounds(alpha, beta, beta_next)
+    lb = theta[0] - resid[0]
+    ub = theta[-1] + resid[-1]
+    if ub <= lb:
+        half = max(abs(ub), 1.0) * 1e-8
+        lb, ub = lb - half, ub + half
+    c, h = 0.5 * (lb + ub), (1.0 + margin) * (0.5 * (ub - lb))  # SpectralInterval.widened (density.py:43-46)
+    return c - h, c + h

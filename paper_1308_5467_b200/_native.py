@@ -93,6 +93,7 @@ SIGNATURES = {
     "sdb_lanczos_workspace_size": (_i, [_p, _i64, _i64, ctypes.POINTER(_sz)]),
     "sdb_lanczos": (_i, [_p, _d, _d, _i64, _i64, _i, _p, _p, _p, _p, _p, _p, _p, _sz, _p]),
     "sdb_ritz_quadrature": (_i, [_p, _p, _p, _i64, _i64, _p, _p, _p]),
+    "sdb_ritz_residual_bounds": (_i, [_p, _p, _p, _i64, _i64, _p, _p, _p]),
     "sdb_pool_nodes": (_i, [_p, _p, _p, _i64, _i64, _d, _p, _p, ctypes.POINTER(_i64), _p]),
     "sdb_blur_nodes": (_i, [_p, _p, _i64, _d, _i, _d, _p, _i64, _p, _p]),
 }

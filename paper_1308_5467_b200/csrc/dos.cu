@@ -112,19 +112,25 @@ __global__ void legendre_series_kernel(const double* __restrict__ c, int64_t deg
 // rotation to a single row vector z (initialised to e_0) instead of a matrix.
 // One block per probe; the serial sweep runs on one thread with d, e, z in
 // shared memory.
+// With resid != NULL the last row zl is rotated as well (initialised to
+// e_{m-1}) and resid = |beta_next| |zl| -- ritz_residual_bounds
+// (lanczos.py:162-167), beta_next read from beta[l][steps_done-1].
 __global__ void ritz_ql_kernel(const double* __restrict__ alpha, const double* __restrict__ beta,
                                const int32_t* __restrict__ steps_done, int64_t m, double* __restrict__ theta,
-                               double* __restrict__ tau2, int* failed) {
+                               double* __restrict__ tau2, double* __restrict__ resid, int* failed) {
   extern __shared__ double sh[];
   double* d = sh;
   double* e = sh + m;
   double* z = sh + 2 * m;
+  double* zl = sh + 3 * m;
+  const bool last = resid != nullptr;
   const int64_t l = blockIdx.x;
   const int64_t mm = steps_done[l];
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
     d[i] = i < mm ? alpha[l * m + i] : 0.0;
     e[i] = (i + 1 < mm) ? beta[l * m + i] : 0.0;
     z[i] = (i == 0) ? 1.0 : 0.0;
+    if (last) zl[i] = (i == mm - 1) ? 1.0 : 0.0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -172,6 +178,11 @@ __global__ void ritz_ql_kernel(const double* __restrict__ alpha, const double* _
             f = z[i + 1];
             z[i + 1] = s * z[i] + c * f;
             z[i] = c * z[i] - s * f;
+            if (last) {
+              f = zl[i + 1];
+              zl[i + 1] = s * zl[i] + c * f;
+              zl[i] = c * zl[i] - s * f;
+            }
           }
           if (deflated) continue;
           d[lo] -= p;
@@ -182,21 +193,25 @@ __global__ void ritz_ql_kernel(const double* __restrict__ alpha, const double* _
     }
     // ascending order (LAPACK convention), insertion sort carrying z
     for (int64_t i = 1; i < nn; ++i) {
-      const double dv = d[i], zv = z[i];
+      const double dv = d[i], zv = z[i], lv = last ? zl[i] : 0.0;
       int64_t j = i - 1;
       while (j >= 0 && d[j] > dv) {
         d[j + 1] = d[j];
         z[j + 1] = z[j];
+        if (last) zl[j + 1] = zl[j];
         --j;
       }
       d[j + 1] = dv;
       z[j + 1] = zv;
+      if (last) zl[j + 1] = lv;
     }
   }
   __syncthreads();
+  const double bn = (last && mm >= 1) ? fabs(beta[l * m + mm - 1]) : 0.0;
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
     theta[l * m + i] = i < mm ? d[i] : 0.0;
-    tau2[l * m + i] = i < mm ? z[i] * z[i] : 0.0;
+    if (tau2) tau2[l * m + i] = i < mm ? z[i] * z[i] : 0.0;
+    if (last) resid[l * m + i] = i < mm ? bn * fabs(zl[i]) : 0.0;
   }
 }
 
@@ -324,18 +339,32 @@ int sdb_legendre_series(const double* c, int64_t degree, const double* t, int64_
   return SDB_OK;
 }
 
+static int ritz_ql(const double* alpha, const double* beta, const int32_t* steps_done, int64_t n_vec, int64_t m,
+                   double* theta, double* tau2, double* resid, void* stream);
+
 int sdb_ritz_quadrature(const double* alpha, const double* beta, const int32_t* steps_done, int64_t n_vec,
                         int64_t m, double* theta, double* tau2, void* stream) {
   SDB_REQUIRE(alpha && beta && steps_done && theta && tau2, "NULL argument");
+  return ritz_ql(alpha, beta, steps_done, n_vec, m, theta, tau2, nullptr, stream);
+}
+
+int sdb_ritz_residual_bounds(const double* alpha, const double* beta, const int32_t* steps_done, int64_t n_vec,
+                             int64_t m, double* theta, double* resid, void* stream) {
+  SDB_REQUIRE(alpha && beta && steps_done && theta && resid, "NULL argument");
+  return ritz_ql(alpha, beta, steps_done, n_vec, m, theta, nullptr, resid, stream);
+}
+
+static int ritz_ql(const double* alpha, const double* beta, const int32_t* steps_done, int64_t n_vec, int64_t m,
+                   double* theta, double* tau2, double* resid, void* stream) {
   SDB_REQUIRE(n_vec >= 1 && m >= 1, "bad shape");
-  size_t shmem = sizeof(double) * 3 * (size_t)m;
+  size_t shmem = sizeof(double) * 4 * (size_t)m;
   SDB_REQUIRE(shmem <= 200 * 1024, "tridiagonal order %lld too large for the on-chip eigensolver", (long long)m);
   cudaStream_t s = (cudaStream_t)stream;
   if (shmem > 48 * 1024) SDB_CUDA(cudaFuncSetAttribute(ritz_ql_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shmem));
   int* failed = nullptr;
   SDB_CUDA(cudaMallocAsync(&failed, sizeof(int), s));
   SDB_CUDA(cudaMemsetAsync(failed, 0, sizeof(int), s));
-  ritz_ql_kernel<<<(unsigned)n_vec, 64, shmem, s>>>(alpha, beta, steps_done, m, theta, tau2, failed);
+  ritz_ql_kernel<<<(unsigned)n_vec, 64, shmem, s>>>(alpha, beta, steps_done, m, theta, tau2, resid, failed);
   cudaError_t le = cudaGetLastError();
   int hf = 0;
   cudaError_t e = le;

@@ -185,6 +185,26 @@ def ritz_quadrature(fact, probe_index=None, device=None):
         return RitzQuadrature(theta=theta[0].cpu().numpy(), tau_sq=tau2[0].cpu().numpy(), probe_index=probe_index)
 
 
+def ritz_residual_bounds(fact, device=None):
+    """Ritz values with their residual bounds beta_next * |last component| (lanczos.py:162-167)."""
+    torch = E._torch()
+    device = E.require_cuda(device)
+    m = int(fact.steps)
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        a = E.to_device(np.asarray(fact.alpha, dtype=float).reshape(1, m), device)
+        b = np.zeros((1, m))
+        b[0, : m - 1] = np.asarray(fact.beta, dtype=float)[: m - 1]
+        b[0, m - 1] = float(fact.beta_next)
+        bd = E.to_device(b, device)
+        sd = torch.tensor([m], dtype=torch.int32, device=device)
+        theta = torch.empty((1, m), dtype=torch.float64, device=device)
+        resid = torch.empty((1, m), dtype=torch.float64, device=device)
+        _native.call("sdb_ritz_residual_bounds", E.ptr(a), E.ptr(bd), E.ptr(sd), 1, m, E.ptr(theta), E.ptr(resid),
+                     stream)
+        return theta[0].cpu().numpy(), resid[0].cpu().numpy()
+
+
 def _pool_device(theta, tau2, steps_done, divisor, device, stream):
     torch = E._torch()
     rows, m = theta.shape

@@ -150,6 +150,43 @@ def variants_case(name, op, kind, n_vec, degree, n_pts):
     return out
 
 
+def interval_case(name):
+    """estimate_spectral_interval (matrix.py:207-241) + ritz_residual_bounds (lanczos.py:162-167)."""
+    from specdens import estimate_spectral_interval
+    from specdens.lanczos import ritz_residual_bounds
+    from specdens.stochastic import INTERVAL_STREAM
+
+    t0 = time.time()
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((20, 20))
+    mats = {
+        "c1": ref_matrix(W.build_matrix("C1")),
+        "c2": ref_matrix(W.build_matrix("C2")),
+        "dense20": SparseSymmetricMatrix.from_dense(a + a.T),
+        "diag10": SparseSymmetricMatrix.from_dense(np.diag(np.arange(1.0, 11.0))),
+        "diag3": SparseSymmetricMatrix.from_dense(np.diag([-3.0, 0.0, 5.0])),
+    }
+    runs = [("c1", 20, 0.01), ("c1", 40, 0.0), ("c2", 20, 0.01), ("dense20", 20, 0.0), ("dense20", 7, 0.05),
+            ("diag10", 10, 0.01), ("diag3", 3, 0.01)]
+    out = {}
+    for i, (key, steps, margin) in enumerate(runs):
+        iv = estimate_spectral_interval(mats[key], lanczos_steps=steps, margin=margin, seed=0)
+        src = ProbeVectorSource("gaussian", seed=0, dim=mats[key].dim, stream=INTERVAL_STREAM)
+        fact = lanczos_factorize(mats[key], src.draw(0), min(steps, mats[key].dim))
+        theta, resid = ritz_residual_bounds(fact)
+        out[f"run{i}_matrix"] = key
+        out[f"run{i}_steps"] = steps
+        out[f"run{i}_margin"] = margin
+        out[f"run{i}_lb"] = iv.lambda_lb
+        out[f"run{i}_ub"] = iv.lambda_ub
+        out[f"run{i}_theta"] = theta
+        out[f"run{i}_resid"] = resid
+    out["runs"] = len(runs)
+    out["dense20"] = a + a.T
+    print(f"{name}: {time.time() - t0:.1f}s", flush=True)
+    return out
+
+
 def main():
     meta = dict(numpy=np.__version__, scipy=scipy.__version__, specdens=specdens.__version__,
                 python=sys.version.split()[0])
@@ -160,6 +197,7 @@ def main():
         "c5_small": lambda: kpm_case("c5_small", W.stencil27_3d(24), "rademacher", 2, 200, 2000),
         "c4_subset": lambda: lanczos_case("c4_subset", W.build_matrix("C4"), "gaussian", 4, 100, 0.01, 2000),
         "lanczos_small": lambda: lanczos_case("lanczos_small", W.anderson_3d(8), "gaussian", 6, 40, 0.05, 400),
+        "interval": lambda: interval_case("interval"),
         "variants_c1": lambda: variants_case("variants_c1", W.build_matrix("C1"), "gaussian", 20, 100, 1000),
         "variants_c5small": lambda: variants_case("variants_c5small", W.stencil27_3d(24), "rademacher", 32, 60,
                                                   500),

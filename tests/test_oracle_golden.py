@@ -115,3 +115,26 @@ def test_oracle_variants_match_reference(golden, name):
     np.testing.assert_array_equal(cheb, g["zeta_chebyshev"])
     np.testing.assert_array_equal(O.spectroscopic_dos(cheb, n, d, t)[1], g["spectroscopic_density"])
     np.testing.assert_array_equal(O.delta_chebyshev_dos(cheb, n, d, t, g["delta_degrees"])[1], g["delta_density"])
+
+
+def _interval_matrices(g):
+    import scipy.sparse as sp
+
+    return {"c1": W.build_matrix("C1").csr, "c2": W.build_matrix("C2").csr, "dense20": sp.csr_array(g["dense20"]),
+            "diag10": sp.csr_array(np.diag(np.arange(1.0, 11.0))), "diag3": sp.csr_array(np.diag([-3.0, 0.0, 5.0]))}
+
+
+def test_oracle_interval_matches_reference(golden):
+    """estimate_spectral_interval / ritz_residual_bounds (matrix.py:207-241, lanczos.py:162-167)."""
+    g = golden("interval")
+    mats = _interval_matrices(g)
+    for i in range(int(g["runs"])):
+        csr = mats[str(g[f"run{i}_matrix"])]
+        steps, margin = int(g[f"run{i}_steps"]), float(g[f"run{i}_margin"])
+        lb, ub = O.estimate_spectral_interval(csr, steps, margin)
+        assert (lb, ub) == (float(g[f"run{i}_lb"]), float(g[f"run{i}_ub"]))
+        v0 = O.draw_probe("gaussian", 0, csr.shape[0], 0, stream=0xB0)
+        a, b, bn, _, _ = O.lanczos_factorize(csr, v0, min(steps, csr.shape[0]))
+        theta, resid = O.ritz_residual_bounds(a, b, bn)
+        np.testing.assert_array_equal(theta, g[f"run{i}_theta"])
+        np.testing.assert_array_equal(resid, g[f"run{i}_resid"])
