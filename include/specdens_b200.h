@@ -224,6 +224,23 @@ SDB_API int sdb_ritz_quadrature(const double* alpha, const double* beta, const i
  * the sdb_lanczos layout).  Outputs n_vec x m; tails zeroed. */
 SDB_API int sdb_ritz_residual_bounds(const double* alpha, const double* beta, const int32_t* steps_done,
                              int64_t n_vec, int64_t m, double* theta, double* resid, void* stream);
+/* haydock_dos (lanczos.py:263-293): per grid point x_i,
+ * density[i] = (1/n_vec) sum_l -Im f_l(x_i + i eta)/pi with f_l the (1,1)
+ * resolvent of probe l's tridiagonal (continued fraction, lanczos.py:222-227),
+ * probes summed in index order; trunc_pts[i] = max_l beta_next_l |w_last|
+ * (Thomas forward sweep, lanczos.py:230-260; beta_next = 0 for probes with
+ * status SDB_LZ_BREAKDOWN) and *trunc = max_i trunc_pts[i] (device scalars;
+ * both may be NULL).  alpha/beta/steps_done/status in the sdb_lanczos layout. */
+SDB_API int sdb_haydock(const double* alpha, const double* beta, const int32_t* steps_done,
+                const int32_t* status, int64_t n_vec, int64_t m, const double* grid, int64_t n_pts,
+                double eta, double* density, double* trunc_pts, double* trunc, void* stream);
+/* continued_fraction_resolvent / tridiagonal_resolvent_first (lanczos.py:222-260)
+ * for one tridiagonal (alpha m, beta m-1) at nz complex points z (interleaved
+ * re, im); outputs interleaved complex, each may be NULL.  scratch: 4*m*nz
+ * doubles when w_first or w_last is requested and m > 1. */
+SDB_API int sdb_tridiag_resolvent(const double* alpha, const double* beta, int64_t m, const double* z,
+                          int64_t nz, double* cf, double* w_first, double* w_last, double* scratch,
+                          void* stream);
 /* pool_ritz_quadratures (lanczos.py:170-177): concatenate the first
  * steps_done[l] entries of every row l of theta/tau2 (n_rows x m), divide the
  * weights by `divisor` (the number of probes) and sort by theta (stable: ties

@@ -357,3 +357,49 @@ def estimate_spectral_interval(matrix, lanczos_steps=20, margin=0.01, seed=0):
         lb, ub = lb - half, ub + half
     c, h = 0.5 * (lb + ub), (1.0 + margin) * (0.5 * (ub - lb))  # SpectralInterval.widened (density.py:43-46)
     return c - h, c + h
+
+
+# ---- lanczos.py:222-293 (Haydock resolvent) ------------------------------------------------------
+def continued_fraction_resolvent(alpha, beta, z):
+    z = np.asarray(z, dtype=complex)
+    f = 1.0 / (z - alpha[-1])
+    for j in range(len(alpha) - 2, -1, -1):
+        f = 1.0 / (z - alpha[j] - beta[j] ** 2 * f)
+    return f
+
+
+def tridiagonal_resolvent_first(alpha, beta, z):
+    z = np.asarray(z, dtype=complex)
+    m = len(alpha)
+    if m == 1:
+        w = 1.0 / (z - alpha[0])
+        return w, w
+    cp = np.empty((m - 1,) + z.shape, dtype=complex)
+    dp = np.empty((m,) + z.shape, dtype=complex)
+    denom = z - alpha[0]
+    cp[0] = -beta[0] / denom
+    dp[0] = 1.0 / denom
+    for j in range(1, m):
+        denom = (z - alpha[j]) + beta[j - 1] * cp[j - 1]
+        if j < m - 1:
+            cp[j] = -beta[j] / denom
+        dp[j] = beta[j - 1] * dp[j - 1] / denom
+    w = dp[m - 1]
+    w_last = w
+    for j in range(m - 2, -1, -1):
+        w = dp[j] - cp[j] * w
+    return w, w_last
+
+
+def haydock_dos(matrix, steps, kind, seed, n_vec, eta, grid, reorth="full"):
+    """(density, truncation_indicator) on the original-coordinate grid."""
+    csr = as_csr(matrix)
+    z = np.asarray(grid, dtype=float) + 1j * eta
+    dens, trunc = [], []
+    for l in range(n_vec):
+        a, b, bn, _, _ = lanczos_factorize(csr, draw_probe(kind, seed, csr.shape[0], l), steps, reorth)
+        f = continued_fraction_resolvent(a, b, z)
+        _, w_last = tridiagonal_resolvent_first(a, b, z)
+        dens.append(-np.imag(f) / np.pi)
+        trunc.append(bn * float(np.max(np.abs(w_last))))
+    return np.mean(dens, axis=0), max(trunc)

@@ -6,9 +6,10 @@ probe mean, finiteness check, coefficients, Clenshaw, 1/sqrt(1-t^2) and the
 1/d unmapping -- stays on the device and the host reads back the moments and
 the density once.  The moment-sharing variants ``spectroscopic``,
 ``delta-cheb`` (same Chebyshev moments) and ``kpml`` (Legendre moments from
-the same fused kernels) run through the same kernels.  The
-remaining reference methods (dgl, haydock, cdos) are outside the accelerated
-path and raise ``NotImplementedError``.
+the same fused kernels) run through the same kernels.  ``haydock``
+evaluates the same batched Lanczos tridiagonals' resolvents on the device
+(§8(f)-3).  The remaining reference methods (dgl, cdos) are outside the
+accelerated path and raise ``NotImplementedError``.
 """
 
 import time
@@ -20,14 +21,14 @@ from . import engine as E
 from . import kpm as K
 from .density import DEFAULT_GRID_POINTS, SpectralDensityEstimate, interval_grid, unit_grid
 from .errors import NumericalFailure
-from .lanczos import lanczos_dos
+from .lanczos import haydock_dos, lanczos_dos
 from .operators import MatvecCounter, apply_spectral_map, as_operator
 
 CHEBYSHEV_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb")
 LEGENDRE_METHODS = ("kpml", "dgl")
 LANCZOS_METHODS = ("lanczos", "haydock", "cdos")
 ALL_METHODS = CHEBYSHEV_METHODS + LEGENDRE_METHODS + LANCZOS_METHODS
-GPU_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb", "kpml", "lanczos")
+GPU_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb", "kpml", "lanczos", "haydock")
 
 
 def analytic_matvec_count(method, degree, n_vec, product_formula=False):
@@ -109,7 +110,10 @@ def estimate_dos(matrix, interval, method, degree, source, n_vec, sigma=None, et
         est = K.evaluate_kpml_dos(moments, interval, unit_grid(grid_points), device=device)
     else:
         grid = interval_grid(interval, grid_points)
-        est = lanczos_dos(counter, interval, degree, source, n_vec, sigma, grid, threads, device=device)
+        if method == "lanczos":
+            est = lanczos_dos(counter, interval, degree, source, n_vec, sigma, grid, threads, device=device)
+        else:
+            est = haydock_dos(counter, interval, degree, source, n_vec, eta, grid, threads, device=device)
     est.params.update({
         "M": degree,
         "n_vec": n_vec,

@@ -215,6 +215,137 @@ __global__ void ritz_ql_kernel(const double* __restrict__ alpha, const double* _
   }
 }
 
+// ---- Haydock resolvent (lanczos.py:222-293), SURVEY §8(f)-3 ---------------------------
+// Complex arithmetic on (re, im) pairs.
+struct cplx {
+  double re, im;
+};
+__device__ __forceinline__ cplx cmk(double r, double i) { return cplx{r, i}; }
+__device__ __forceinline__ cplx csub(cplx a, cplx b) { return cplx{a.re - b.re, a.im - b.im}; }
+__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return cplx{a.re + b.re, a.im + b.im}; }
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) { return cplx{a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re}; }
+__device__ __forceinline__ cplx cscale(double s, cplx a) { return cplx{s * a.re, s * a.im}; }
+// a / b, Smith's algorithm (the scaling NumPy's complex division uses)
+__device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
+  if (fabs(b.re) >= fabs(b.im)) {
+    if (b.re == 0.0 && b.im == 0.0) return cplx{a.re / fabs(b.re), a.im / fabs(b.im)};
+    const double r = b.im / b.re, den = b.re + b.im * r;
+    return cplx{(a.re + a.im * r) / den, (a.im - a.re * r) / den};
+  }
+  const double r = b.re / b.im, den = b.im + b.re * r;
+  return cplx{(a.re * r + a.im) / den, (a.im * r - a.re) / den};
+}
+__device__ __forceinline__ double cabs_(cplx a) { return hypot(a.re, a.im); }
+
+// e1^T (zI - T)^{-1} e1 by the bottom-up continued fraction (lanczos.py:222-227).
+__device__ cplx cf_resolvent(const double* a, const double* b, int64_t mm, cplx z) {
+  const cplx one = cmk(1.0, 0.0);
+  cplx f = cdiv(one, csub(z, cmk(a[mm - 1], 0.0)));
+  for (int64_t j = mm - 2; j >= 0; --j) f = cdiv(one, csub(csub(z, cmk(a[j], 0.0)), cscale(b[j] * b[j], f)));
+  return f;
+}
+
+// Last entry of the Thomas solve of (zI - T) w = e1 (lanczos.py:230-260, forward sweep).
+__device__ cplx thomas_last(const double* a, const double* b, int64_t mm, cplx z) {
+  const cplx one = cmk(1.0, 0.0);
+  if (mm == 1) return cdiv(one, csub(z, cmk(a[0], 0.0)));
+  cplx denom = csub(z, cmk(a[0], 0.0));
+  cplx cp = cdiv(cmk(-b[0], 0.0), denom);
+  cplx dp = cdiv(one, denom);
+  for (int64_t j = 1; j < mm; ++j) {
+    denom = cadd(csub(z, cmk(a[j], 0.0)), cscale(b[j - 1], cp));
+    const cplx cpn = (j < mm - 1) ? cdiv(cmk(-b[j], 0.0), denom) : cp;
+    dp = cdiv(cscale(b[j - 1], dp), denom);
+    cp = cpn;
+  }
+  return dp;
+}
+
+// haydock_dos (lanczos.py:263-293): density(x) = mean_l -Im f_l(x + i eta)/pi in
+// probe order; trunc[i] = max_l beta_next_l |w_last,l(x_i + i eta)|.  One grid
+// point per thread, every probe's tridiagonal walked in order.
+__global__ void haydock_kernel(const double* __restrict__ alpha, const double* __restrict__ beta,
+                               const int32_t* __restrict__ steps_done, const int32_t* __restrict__ status,
+                               int64_t n_vec, int64_t m, const double* __restrict__ grid, int64_t n_pts, double eta,
+                               double* __restrict__ density, double* __restrict__ trunc) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_pts) return;
+  const cplx z = cmk(grid[i], eta);
+  double sum = 0.0, tmax = 0.0;
+  for (int64_t l = 0; l < n_vec; ++l) {
+    const int64_t mm = steps_done[l];
+    const double* a = alpha + l * m;
+    const double* b = beta + l * m;
+    const cplx f = cf_resolvent(a, b, mm, z);
+    sum += -f.im / M_PI;
+    const cplx wl = thomas_last(a, b, mm, z);
+    const double bn = status[l] == SDB_LZ_BREAKDOWN ? 0.0 : b[mm - 1];
+    const double tv = bn * cabs_(wl);
+    tmax = tv > tmax ? tv : tmax;
+  }
+  density[i] = sum / (double)n_vec;
+  if (trunc) trunc[i] = tmax;
+}
+
+// continued_fraction_resolvent / tridiagonal_resolvent_first for one
+// tridiagonal at arbitrary complex points (z interleaved re, im).  The back
+// substitution for w_0 keeps cp, dp per point in scratch (2 m complex each).
+__global__ void tridiag_resolvent_kernel(const double* __restrict__ alpha, const double* __restrict__ beta,
+                                         int64_t m, const double* __restrict__ zs, int64_t nz,
+                                         double* __restrict__ cf, double* __restrict__ wfirst,
+                                         double* __restrict__ wlast, double* __restrict__ scratch) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= nz) return;
+  const cplx z = cmk(zs[2 * i], zs[2 * i + 1]);
+  const cplx one = cmk(1.0, 0.0);
+  if (cf) {
+    const cplx f = cf_resolvent(alpha, beta, m, z);
+    cf[2 * i] = f.re;
+    cf[2 * i + 1] = f.im;
+  }
+  if (!wfirst && !wlast) return;
+  cplx w0, wl;
+  if (m == 1) {
+    w0 = wl = cdiv(one, csub(z, cmk(alpha[0], 0.0)));
+  } else {
+    cplx* cpa = reinterpret_cast<cplx*>(scratch) + i * 2 * m;
+    cplx* dpa = cpa + m;
+    cplx denom = csub(z, cmk(alpha[0], 0.0));
+    cpa[0] = cdiv(cmk(-beta[0], 0.0), denom);
+    dpa[0] = cdiv(one, denom);
+    for (int64_t j = 1; j < m; ++j) {
+      denom = cadd(csub(z, cmk(alpha[j], 0.0)), cscale(beta[j - 1], cpa[j - 1]));
+      if (j < m - 1) cpa[j] = cdiv(cmk(-beta[j], 0.0), denom);
+      dpa[j] = cdiv(cscale(beta[j - 1], dpa[j - 1]), denom);
+    }
+    wl = dpa[m - 1];
+    cplx w = wl;
+    for (int64_t j = m - 2; j >= 0; --j) w = csub(dpa[j], cmul(cpa[j], w));
+    w0 = w;
+  }
+  if (wfirst) {
+    wfirst[2 * i] = w0.re;
+    wfirst[2 * i + 1] = w0.im;
+  }
+  if (wlast) {
+    wlast[2 * i] = wl.re;
+    wlast[2 * i + 1] = wl.im;
+  }
+}
+
+__global__ void max_reduce_kernel(const double* __restrict__ x, int64_t n, double* __restrict__ out) {
+  __shared__ double red[256];
+  double v = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) v = x[i] > v ? x[i] : v;
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s && red[threadIdx.x + s] > red[threadIdx.x]) red[threadIdx.x] = red[threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = red[0];
+}
+
 // ---- node pooling (lanczos.py:170-177) ---------------------------------------------
 // Stable rank sort of the concatenated nodes: rank(i) = #{j : th_j < th_i} +
 // #{j < i : th_j == th_i}.  O(N^2) compares on a tile of theta staged in
@@ -335,6 +466,38 @@ int sdb_legendre_series(const double* c, int64_t degree, const double* t, int64_
   SDB_REQUIRE(density == nullptr || divisor != 0.0, "divisor must be non-zero");
   int blocks = (int)((n_pts + 127) / 128);
   legendre_series_kernel<<<blocks, 128, 0, (cudaStream_t)stream>>>(c, degree, t, n_pts, divisor, values, density);
+  SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+int sdb_haydock(const double* alpha, const double* beta, const int32_t* steps_done, const int32_t* status,
+                int64_t n_vec, int64_t m, const double* grid, int64_t n_pts, double eta, double* density,
+                double* trunc_pts, double* trunc, void* stream) {
+  SDB_REQUIRE(alpha && beta && steps_done && status && grid && density, "NULL argument");
+  SDB_REQUIRE(n_vec >= 1 && m >= 1, "bad shape");
+  SDB_REQUIRE(eta > 0.0, "eta must be positive");
+  SDB_REQUIRE(trunc == nullptr || trunc_pts != nullptr, "trunc needs the per-point buffer");
+  if (n_pts <= 0) return SDB_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  haydock_kernel<<<(unsigned)((n_pts + 127) / 128), 128, 0, s>>>(alpha, beta, steps_done, status, n_vec, m, grid,
+                                                                  n_pts, eta, density, trunc_pts);
+  SDB_CHECK_LAUNCH();
+  if (trunc) {
+    max_reduce_kernel<<<1, 256, 0, s>>>(trunc_pts, n_pts, trunc);
+    SDB_CHECK_LAUNCH();
+  }
+  return SDB_OK;
+}
+
+int sdb_tridiag_resolvent(const double* alpha, const double* beta, int64_t m, const double* z, int64_t nz,
+                          double* cf, double* w_first, double* w_last, double* scratch, void* stream) {
+  SDB_REQUIRE(alpha && z, "NULL argument");
+  SDB_REQUIRE(m >= 1, "bad shape");
+  SDB_REQUIRE(m == 1 || (beta != nullptr && (scratch != nullptr || (!w_first && !w_last))),
+              "beta / scratch required");
+  if (nz <= 0) return SDB_OK;
+  tridiag_resolvent_kernel<<<(unsigned)((nz + 127) / 128), 128, 0, (cudaStream_t)stream>>>(alpha, beta, m, z, nz, cf,
+                                                                                           w_first, w_last, scratch);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }

@@ -325,3 +325,112 @@ def lanczos_dos(op, interval, steps, source, n_vec, sigma, grid=None, threads=No
         grid, density, grid, density, interval, method="lanczos",
         params={"M": steps, "n_vec": n_vec, "sigma": sigma, "ritz_nodes": nodes_h, "ritz_weights": weights_h},
     )
+
+
+# ---------------------------------------------------------------------------
+# Haydock resolvent (lanczos.py:222-293): the batched
+# Lanczos tridiagonals stay on the device and one kernel evaluates every
+# probe's continued fraction and truncation diagnostic per grid point.
+
+
+def lanczos_tridiagonals_device(op, steps, source, n_vec, reorth="full", device=None, probes=None):
+    """All probes' (alpha, beta, steps_done, status) on device (sdb_lanczos layout)."""
+    torch = E._torch()
+    device = E.require_cuda(device)
+    res = resolve(op)
+    n = res.dim
+    _check_args(reorth, steps, n)
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        dm = device_matrix(res.base, device, stream)
+        alpha = torch.empty((n_vec, steps), dtype=torch.float64, device=device)
+        beta = torch.empty((n_vec, steps), dtype=torch.float64, device=device)
+        sd_all = torch.empty(n_vec, dtype=torch.int32, device=device)
+        st_all = torch.empty(n_vec, dtype=torch.int32, device=device)
+        for start, count in E.batches(n_vec, _batch_size(n, steps, n_vec)):
+            if probes is not None:
+                staged = E.pack_device_probes(probes[start:start + count], device, stream)
+            else:
+                staged = E.stage_probes(source, start, count, n, device, stream)
+            out = _run_batch(dm, res, staged, count, steps, reorth, device, stream)
+            out.basis = None
+            alpha[start:start + count] = out.alpha
+            beta[start:start + count] = out.beta
+            sd_all[start:start + count] = out.steps_done
+            st_all[start:start + count] = out.status
+        status = st_all.cpu().numpy()
+        sd = sd_all.cpu().numpy()
+    _raise_for_status(status, sd)
+    return res, alpha, beta, sd_all, st_all
+
+
+def _resolvent(alpha, beta, z, want_cf, want_w, device=None):
+    torch = E._torch()
+    device = E.require_cuda(device)
+    alpha = np.asarray(alpha, dtype=float)
+    beta = np.asarray(beta, dtype=float)
+    z = np.asarray(z, dtype=complex)
+    m = len(alpha)
+    zf = np.ascontiguousarray(z.ravel())
+    nz = zf.size
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        a = E.to_device(alpha, device)
+        b = E.to_device(beta if m > 1 else np.zeros(1), device)
+        zd = E.to_device(zf.view(np.float64), device)
+        cf = torch.empty(2 * nz, dtype=torch.float64, device=device) if want_cf else None
+        w0 = torch.empty(2 * nz, dtype=torch.float64, device=device) if want_w else None
+        wl = torch.empty(2 * nz, dtype=torch.float64, device=device) if want_w else None
+        scratch = torch.empty(max(4 * m * nz, 1), dtype=torch.float64, device=device) if want_w else None
+        _native.call("sdb_tridiag_resolvent", E.ptr(a), E.ptr(b), m, E.ptr(zd), nz, E.ptr(cf), E.ptr(w0), E.ptr(wl),
+                     E.ptr(scratch), stream)
+
+        def host(t):
+            return None if t is None else t.cpu().numpy().view(np.complex128).reshape(z.shape)
+
+        return host(cf), host(w0), host(wl)
+
+
+def continued_fraction_resolvent(alpha, beta, z, device=None):
+    """Bottom-up continued fraction for e1^T (zI - T)^{-1} e1, vectorized in z (lanczos.py:222-227)."""
+    return _resolvent(alpha, beta, z, True, False, device)[0]
+
+
+def tridiagonal_resolvent_first(alpha, beta, z, device=None):
+    """(w_0, w_{M-1}) of (zI - T) w = e1 by the Thomas algorithm (lanczos.py:230-260)."""
+    _, w0, wl = _resolvent(alpha, beta, z, False, True, device)
+    return w0, wl
+
+
+def haydock_dos(op, interval, steps, source, n_vec, eta=None, grid=None, threads=None, reorth="full", device=None):
+    """Lorentzian-regularized DOS from the (1,1) resolvent continued fraction (lanczos.py:263-293).
+
+    ``eta`` defaults to half a grid spacing; params["truncation_indicator"] is
+    max beta_next |w_{M-1}| over probes and grid points.
+    """
+    if grid is None:
+        grid = interval_grid(interval, DEFAULT_GRID_POINTS)
+    grid = np.asarray(grid, dtype=float)
+    if eta is None:
+        eta = interval.width / (2.0 * len(grid))
+    if not eta > 0:
+        raise ValueError("eta must be positive")
+    torch = E._torch()
+    device = E.require_cuda(device)
+    res, alpha, beta, sd, st = lanczos_tridiagonals_device(op, steps, source, n_vec, reorth=reorth, device=device)
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        g = E.to_device(grid, device)
+        dens = torch.empty_like(g)
+        tpts = torch.empty_like(g)
+        trunc = torch.empty(1, dtype=torch.float64, device=device)
+        _native.call("sdb_haydock", E.ptr(alpha), E.ptr(beta), E.ptr(sd), E.ptr(st), n_vec, steps, E.ptr(g),
+                     g.numel(), float(eta), E.ptr(dens), E.ptr(tpts), E.ptr(trunc), stream)
+        packed = torch.cat([dens, trunc]).cpu().numpy()
+    for c in res.counters:
+        c.count += int(sd.sum().item())
+    density = packed[:-1]
+    return SpectralDensityEstimate.from_original(
+        grid, density, interval, method="haydock",
+        params={"M": steps, "n_vec": n_vec, "eta": eta, "truncation_indicator": float(packed[-1])},
+    )

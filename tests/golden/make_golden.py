@@ -187,6 +187,32 @@ def interval_case(name):
     return out
 
 
+def haydock_case(name, op, kind, n_vec, steps, n_pts, eta):
+    """haydock_dos (lanczos.py:263-293) and the resolvent routes (lanczos.py:222-260)."""
+    from specdens.lanczos import continued_fraction_resolvent, haydock_dos, tridiagonal_resolvent_first
+
+    t0 = time.time()
+    mat = ref_matrix(op)
+    g = W.gershgorin_interval(op)
+    iv = SpectralInterval(g.lambda_lb, g.lambda_ub)
+    src = ProbeVectorSource(kind, seed=0, dim=mat.dim)
+    grid = interval_grid(iv, n_pts)
+    est = haydock_dos(mat, iv, steps, src, n_vec, eta=eta, grid=grid)
+    est_default = haydock_dos(mat, iv, steps, src, n_vec, grid=grid)
+    est2 = estimate_dos(mat, iv, "haydock", steps, src, n_vec, eta=eta, grid_points=n_pts)
+    fact = lanczos_factorize(mat, src.draw(0), steps)
+    z = np.linspace(iv.lambda_lb - 1.0, iv.lambda_ub + 1.0, 300) + 1j * eta
+    cf = continued_fraction_resolvent(fact.alpha, fact.beta, z)
+    w0, wl = tridiagonal_resolvent_first(fact.alpha, fact.beta, z)
+    print(f"{name}: n={mat.dim} {time.time() - t0:.1f}s", flush=True)
+    return dict(kind=kind, n_vec=n_vec, steps=steps, n_pts=n_pts, eta=eta, lb=iv.lambda_lb, ub=iv.lambda_ub,
+                grid=grid, density=est.density, trunc=est.params["truncation_indicator"],
+                density_default_eta=est_default.density, default_eta=est_default.params["eta"],
+                trunc_default=est_default.params["truncation_indicator"], estimate_density=est2.density,
+                estimate_matvec_count=est2.params["matvec_count"], alpha0=fact.alpha, beta0=fact.beta, z=z, cf=cf,
+                w_first=w0, w_last=wl, matrix_sha256=csr_digest(mat.csr), n=mat.dim)
+
+
 def main():
     meta = dict(numpy=np.__version__, scipy=scipy.__version__, specdens=specdens.__version__,
                 python=sys.version.split()[0])
@@ -197,6 +223,8 @@ def main():
         "c5_small": lambda: kpm_case("c5_small", W.stencil27_3d(24), "rademacher", 2, 200, 2000),
         "c4_subset": lambda: lanczos_case("c4_subset", W.build_matrix("C4"), "gaussian", 4, 100, 0.01, 2000),
         "lanczos_small": lambda: lanczos_case("lanczos_small", W.anderson_3d(8), "gaussian", 6, 40, 0.05, 400),
+        "haydock_small": lambda: haydock_case("haydock_small", W.anderson_3d(8), "gaussian", 6, 40, 400, 0.05),
+        "haydock_c4": lambda: haydock_case("haydock_c4", W.build_matrix("C4"), "gaussian", 4, 100, 2000, 0.01),
         "interval": lambda: interval_case("interval"),
         "variants_c1": lambda: variants_case("variants_c1", W.build_matrix("C1"), "gaussian", 20, 100, 1000),
         "variants_c5small": lambda: variants_case("variants_c5small", W.stencil27_3d(24), "rademacher", 32, 60,

@@ -99,7 +99,7 @@ def test_validation_happens_before_any_device_work():
     with pytest.raises(ValueError, match="product formula"):
         sdb.estimate_dos(a, sdb.SpectralInterval(0, 2), "lanczos", 4, src, 1, sigma=0.1, product_formula=True)
     with pytest.raises(NotImplementedError):
-        sdb.estimate_dos(a, sdb.SpectralInterval(0, 2), "haydock", 4, src, 1)
+        sdb.estimate_dos(a, sdb.SpectralInterval(0, 2), "cdos", 4, src, 1)
     with pytest.raises(ValueError):
         sdb.lanczos_factorize(a, np.ones(3), 4)
     with pytest.raises(ValueError):

@@ -138,3 +138,29 @@ def test_oracle_interval_matches_reference(golden):
         theta, resid = O.ritz_residual_bounds(a, b, bn)
         np.testing.assert_array_equal(theta, g[f"run{i}_theta"])
         np.testing.assert_array_equal(resid, g[f"run{i}_resid"])
+
+
+HAYDOCK_CASES = {"haydock_small": lambda: W.anderson_3d(8), "haydock_c4": lambda: W.build_matrix("C4")}
+
+
+@pytest.mark.parametrize("name", list(HAYDOCK_CASES))
+def test_oracle_haydock_matches_reference(golden, name):
+    """haydock_dos + resolvent routes (lanczos.py:222-293)."""
+    g = golden(name)
+    if name == "haydock_c4":
+        # the full run takes ~1 min of CPU: check the resolvent routes only
+        np.testing.assert_array_equal(O.continued_fraction_resolvent(g["alpha0"], g["beta0"], g["z"]), g["cf"])
+        w0, wl = O.tridiagonal_resolvent_first(g["alpha0"], g["beta0"], g["z"])
+        np.testing.assert_array_equal(w0, g["w_first"])
+        np.testing.assert_array_equal(wl, g["w_last"])
+        return
+    op = HAYDOCK_CASES[name]()
+    assert csr_digest(op.csr) == str(g["matrix_sha256"])
+    dens, trunc = O.haydock_dos(op.csr, int(g["steps"]), str(g["kind"]), 0, int(g["n_vec"]), float(g["eta"]),
+                                g["grid"])
+    np.testing.assert_array_equal(dens, g["density"])
+    assert trunc == float(g["trunc"])
+    np.testing.assert_array_equal(O.continued_fraction_resolvent(g["alpha0"], g["beta0"], g["z"]), g["cf"])
+    w0, wl = O.tridiagonal_resolvent_first(g["alpha0"], g["beta0"], g["z"])
+    np.testing.assert_array_equal(w0, g["w_first"])
+    np.testing.assert_array_equal(wl, g["w_last"])
