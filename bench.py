@@ -137,6 +137,7 @@ def kernel_label(dm, n_vec, mode):
 
     name = _native.load().sdb_cheb_kernel(dm.handle, n_vec, mode).decode()
     detail = {"cheb_step_zmarch": "TMA z-march, ghost-padded planes, register-rolled z terms",
+              "cheb_step2_zmarch": "TMA z-march, two fused steps per launch (temporal blocking)",
               "cheb_step_tile": "2.5-D cp.async shared-memory tiles",
               "cheb_step_grid": "row panels", "cheb_step_csr": "CSR row groups",
               "cheb_step_stencil": "generic stencil"}.get(name, "")
@@ -365,15 +366,25 @@ def main():
 
     # ---- roofline of the dominant kernel (the fused recurrence step) ----
     dm = run.dm
-    launches = steps_per_probe
     ldv = E.block_ldv(n_vec)
-    bytes_launch = dm.bytes_per_pass + 24 * n * n_vec + (8 * n * n_vec if not product else 0)
-    avg_launch_s = k_ms * 1e-3 / launches
-    achieved = bytes_launch / avg_launch_s / 1e9
-    peak, peak_kind = load_peaks()
     mode_c = _native.SDB_CHEB_DOUBLING if product else _native.SDB_CHEB_DIRECT
     klabel = kernel_label(dm, n_vec, mode_c)
     kname = klabel.split(" ")[0]
+    one_step = dm.bytes_per_pass + 24 * n * n_vec + (8 * n * n_vec if not product else 0)
+    if kname == "cheb_step2_zmarch":
+        # fused pairs: per launch the diagonal once, w_k and w_{k-1} read,
+        # w_{k+1} and w_{k+2} written; an odd step count ends with one step
+        pairs, singles = steps_per_probe // 2, steps_per_probe % 2
+        bytes_launch = dm.bytes_per_pass + 32 * n * n_vec
+        launches = pairs + singles
+        total_bytes = pairs * bytes_launch + singles * one_step
+    else:
+        bytes_launch = one_step
+        launches = steps_per_probe
+        total_bytes = launches * one_step
+    avg_launch_s = k_ms * 1e-3 / launches
+    achieved = total_bytes / (k_ms * 1e-3) / 1e9
+    peak, peak_kind = load_peaks()
     traffic = load_traffic(args.config, args.format, kname)
     internal = ("stencil (detected from CSR)" if dm.detected_stencil else
                 ("stencil" if dm.format == _native.SDB_FMT_STENCIL else "csr"))
@@ -392,7 +403,8 @@ def main():
 
     # my kernels per step: pack + recurrence steps + 2-stage reduce + mean + coefficients + series
     # (+1 ghost-padding copy of the probes on the z-march path)
-    gpu_launches = args.steps * (1 + launches + 2 + 1 + 1 + 1 + (1 if kname == "cheb_step_zmarch" else 0))
+    zm_extra = {"cheb_step_zmarch": 1, "cheb_step2_zmarch": 2}.get(kname, 0)  # probe (+ diagonal) padding
+    gpu_launches = args.steps * (1 + launches + 2 + 1 + 1 + 1 + zm_extra)
     line = {
         "metric": "Chebyshev moment steps: nnz*n_vec*deg/s (GNNZ-vec/s)",
         "value": value, "unit": "GNNZ-vec/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

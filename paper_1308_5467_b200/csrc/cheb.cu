@@ -763,8 +763,9 @@ int sdb_cheb_workspace_size(const sdb_matrix* m, int64_t n_vec, int64_t degree, 
   ZmPlan zp;
   int rc = zm_plan(m, g.ldv, mode, &zp);
   if (rc) return rc;
-  // z-march path: padded probe copy + two padded recurrence buffers
-  *bytes = zp.on ? 3 * zp.block_bytes + pb : 2 * bb + pb;
+  // z-march path: padded probe copy + two padded recurrence buffers (fused
+  // pairs: + a third and the padded diagonal)
+  *bytes = !zp.on ? 2 * bb + pb : (zp.fuse ? 4 * zp.block_bytes + zp.diag_bytes + pb : 3 * zp.block_bytes + pb);
   return SDB_OK;
 }
 
@@ -809,7 +810,9 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
   double* bufA = (double*)workspace;
   double* bufB = (double*)((char*)workspace + blk);
   double* padded = zp.on ? (double*)((char*)workspace + 2 * blk) : nullptr;
-  double* partials = (double*)((char*)workspace + (zp.on ? 3 : 2) * blk);
+  double* bufC = zp.fuse ? (double*)((char*)workspace + 3 * blk) : nullptr;
+  double* diag_padded = zp.fuse ? (double*)((char*)workspace + 4 * blk) : nullptr;
+  double* partials = (double*)((char*)workspace + (zp.fuse ? 4 * blk + zp.diag_bytes : (zp.on ? 3 : 2) * blk));
 
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (step_ms) {
@@ -824,8 +827,44 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
   }
   const double* cur = v0;
   const double* prev = nullptr;
-  for (int64_t k = 0; k < (steps > 0 ? steps : 1); ++k) {
-    double* next = (k == 0) ? bufA : (k == 1 ? bufB : const_cast<double*>(prev));
+  int64_t k0 = 0;
+  if (zp.on && zp.fuse) {
+    // fused pairs of steps; buffers rotate over {padded, A, B, C} (each pair
+    // writes two buffers distinct from its x and prev)
+    if ((rc = zm_pad_diag(m, diag_padded, s))) return rc;
+    double* pool[4] = {padded, bufA, bufB, bufC};
+    auto clip = [&](int64_t slot) { return slot <= degree ? (int)slot : -1; };
+    for (; k0 + 1 < steps; k0 += 2) {
+      double* outs[2];
+      int no = 0;
+      for (int i = 0; i < 4 && no < 2; ++i)
+        if (pool[i] != cur && pool[i] != prev) outs[no++] = pool[i];
+      StepArgs a = P.a;
+      a.partials = partials;
+      a.v0 = v0;
+      a.x = cur;
+      a.prev = prev;
+      a.next = outs[0];
+      a.next2 = outs[1];
+      a.slot0 = (k0 == 0) ? 0 : -1;
+      a.slotB = clip(2 * k0 + 1);
+      a.slotA = clip(2 * k0 + 2);
+      a.slotB2 = clip(2 * k0 + 3);
+      a.slotA2 = clip(2 * k0 + 4);
+      if ((rc = zm_launch_pair(m, zp, a, diag_padded, k0 == 0, s))) return rc;
+      prev = outs[0];
+      cur = outs[1];
+    }
+    if (k0 < steps) {  // odd step count: one single step, written over a free buffer
+      double* out = nullptr;
+      for (int i = 0; i < 4 && !out; ++i)
+        if (pool[i] != cur && pool[i] != prev) out = pool[i];
+      bufA = out;  // picked up as `next` by the loop below (k0 >= 1 -> k0 != 1 handled there)
+    }
+  }
+  for (int64_t k = k0; k < (steps > 0 ? steps : 1); ++k) {
+    double* next = (k == 0 || (zp.fuse && k == k0 && k0 > 0)) ? bufA
+                   : (k == 1 ? bufB : const_cast<double*>(prev));
     if (zp.on) {
       StepArgs a = P.a;
       a.partials = partials;

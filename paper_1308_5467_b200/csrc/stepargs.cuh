@@ -25,6 +25,10 @@ struct StepArgs {
   // w_{k+1} = (la t - lb w_{k-1}) / lc with la = 2k+1, lb = k, lc = k+1
   int legendre;
   double la, lb, lc;
+  // fused two-step z-march (zmarch.cu): w_{k+2} and its moment slots
+  double* next2;
+  int slotA2;          // <w++,w++>  (-1: none)
+  int slotB2;          // <w++,w+>   (-1: none)
 };
 
 // SDB_LEGENDRE runs the direct-mode kernels with the Legendre update.
@@ -61,7 +65,7 @@ struct GridShape<SDB_SHAPE_BOX27> {
 
 // ---- TMA z-march path (zmarch.cu) ------------------------------------------------
 // Plan for sdb_cheb_moments on a periodic 7/27-point grid: the recurrence
-// buffers are ghost-padded blocks [nz][ny+2][nx+2][ldv] (zm_block_bytes each).
+// buffers are ghost-padded blocks [nz][ny+4][nx+4][ldv] (zm_block_bytes each).
 struct ZmPlan {
   bool on = false;
   int cfg = -1;          // tile configuration (CS, TX, TY, PPT)
@@ -73,11 +77,22 @@ struct ZmPlan {
   int64_t nbp = 0;       // partial rows = grid / slices
   size_t smem = 0;
   size_t block_bytes = 0;
+  size_t diag_bytes = 0;   // padded diagonal (fused pairs)
+  bool fuse = false;       // fused two-step launches (doubling mode)
+  size_t smem2 = 0;        // their dynamic shared memory
+  int R2 = 0;              // and ring depth
   const char* name = "";
 };
 int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* p);
 // w_{k+1} = step(x = w_k, prev = w_{k-1}) on padded blocks; partial rows p.nbp.
 int zm_launch_step(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, bool first, int mode, cudaStream_t s);
+// Fused pair of doubling-mode steps k, k+1: x = w_k, prev = w_{k-1} (unused
+// when first) -> next = w_{k+1}, next2 = w_{k+2} (padded blocks distinct from
+// x and prev); diag_padded from zm_pad_diag.
+int zm_launch_pair(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, const double* diag_padded, bool first,
+                   cudaStream_t s);
+// diagonal (n) -> ghost-padded [nz][ny+4][nx+4]
+int zm_pad_diag(const sdb_matrix* m, double* padded, cudaStream_t s);
 // probes (n x ldv) -> padded block
 int zm_pad(const sdb_matrix* m, const double* probes, int64_t ldv, double* padded, cudaStream_t s);
 

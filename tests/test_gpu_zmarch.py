@@ -17,6 +17,7 @@ from paper_1308_5467_b200.operators import StencilOperator
 pytestmark = pytest.mark.gpu
 
 MOMENT_RTOL = 1e-10
+ZMARCH = ("cheb_step_zmarch", "cheb_step2_zmarch")
 FACE = [(-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)]
 
 
@@ -74,12 +75,12 @@ def test_zmarch_matches_oracle_and_grid_kernel(monkeypatch, shape, kind, n_vec, 
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     for mode, omode in ((_native.SDB_CHEB_DOUBLING, "doubling"), (_native.SDB_CHEB_DIRECT, "direct")):
-        assert kernel_name(op, n_vec, mode) == "cheb_step_zmarch"
+        assert kernel_name(op, n_vec, mode) in ZMARCH
         z = per_probe(op, iv, degree, src, n_vec, mode)
         ref = np.array(O.chebyshev_moments(op, iv.center, iv.halfwidth, degree, "gaussian", 1, n_vec, mode=omode))
         assert rel(z, ref) <= MOMENT_RTOL, (mode, rel(z, ref))
         monkeypatch.setenv("SDB_ZMARCH", "0")
-        assert kernel_name(op, n_vec, mode) != "cheb_step_zmarch"
+        assert kernel_name(op, n_vec, mode) not in ZMARCH
         zg = per_probe(op, iv, degree, src, n_vec, mode)
         monkeypatch.delenv("SDB_ZMARCH")
         # same w_{k+1} bits; only the dot-product reduction trees differ
@@ -118,3 +119,41 @@ def test_zmarch_estimate_dos_end_to_end():
     assert rel(est.params["moments"], zeta) <= MOMENT_RTOL
     _, dens = O.evaluate_kpm_dos(O.moments_to_coefficients(zeta, op.dim, "jackson"), iv.halfwidth, O.unit_grid(300))
     assert np.max(np.abs(est.density - dens)) <= 1e-9
+
+
+# fused pairs (cheb_step2_zmarch, doubling mode, opt-in) against single z-march steps:
+# same w bits, so moments agree to the reduction-order level; every step-count
+# parity (degree 1..4 and odd/even tails), both shapes, every fused tile config
+FUSED_CASES = [
+    ((16, 16, 8), "face7", 64, 3, 17),
+    ((16, 16, 8), "box27", 64, 3, 16),
+    ((16, 16, 9), "box27", 32, 0, 3),
+    ((32, 8, 6), "face7", 16, 2, 4),
+    ((8, 8, 5), "box27", 8, 5, 2),
+    ((8, 8, 4), "face7", 8, 5, 1),
+    ((16, 8, 12), "box27", 16, 0, 23),
+]
+
+
+@pytest.mark.parametrize("shape,kind,n_vec,cfg,degree", FUSED_CASES)
+def test_fused_pairs_match_single_steps(monkeypatch, shape, kind, n_vec, cfg, degree):
+    op = make_stencil(shape, kind, seed=7 + n_vec)
+    iv = W.gershgorin_interval(op)
+    src = sdb.ProbeVectorSource("gaussian", seed=3, dim=op.dim)
+    mode = _native.SDB_CHEB_DOUBLING
+    monkeypatch.setenv("SDB_ZM_CFG", str(cfg))
+    monkeypatch.setenv("SDB_ZM_FUSE", "1")
+    assert kernel_name(op, n_vec, mode) == "cheb_step2_zmarch"
+    z = per_probe(op, iv, degree, src, n_vec, mode)
+    ref = np.array(O.chebyshev_moments(op, iv.center, iv.halfwidth, degree, "gaussian", 3, n_vec, mode="doubling"))
+    assert rel(z, ref) <= MOMENT_RTOL
+    monkeypatch.setenv("SDB_ZM_FUSE", "0")
+    assert kernel_name(op, n_vec, mode) == "cheb_step_zmarch"
+    z1 = per_probe(op, iv, degree, src, n_vec, mode)
+    assert rel(z, z1) <= 1e-13
+    # segmented z with a short ring
+    monkeypatch.setenv("SDB_ZM_FUSE", "1")
+    monkeypatch.setenv("SDB_ZM_NZS", "2")
+    monkeypatch.setenv("SDB_ZM_R2", "4")
+    z2 = per_probe(op, iv, degree, src, n_vec, mode)
+    assert rel(z2, z1) <= 1e-13
