@@ -822,7 +822,7 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
   }
   const double* v0 = probes;
   if (zp.on) {  // ghost-padded copy of the probes (counted in the step time)
-    if ((rc = zm_pad(m, probes, P.g.ldv, padded, s))) return rc;
+    if ((rc = zm_pad(m, zp, probes, P.g.ldv, padded, s))) return rc;
     v0 = padded;
   }
   const double* cur = v0;

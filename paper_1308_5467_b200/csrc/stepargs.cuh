@@ -65,7 +65,7 @@ struct GridShape<SDB_SHAPE_BOX27> {
 
 // ---- TMA z-march path (zmarch.cu) ------------------------------------------------
 // Plan for sdb_cheb_moments on a periodic 7/27-point grid: the recurrence
-// buffers are ghost-padded blocks [nz][ny+4][nx+4][ldv] (zm_block_bytes each).
+// buffers are ghost-padded blocks [nz][ny+2G][nx+2G][ldv] (block_bytes each).
 struct ZmPlan {
   bool on = false;
   int cfg = -1;          // tile configuration (CS, TX, TY, PPT)
@@ -81,6 +81,7 @@ struct ZmPlan {
   bool fuse = false;       // fused two-step launches (doubling mode)
   size_t smem2 = 0;        // their dynamic shared memory
   int R2 = 0;              // and ring depth
+  int G = 1;               // ghost width of the padded blocks (2 with fused pairs)
   const char* name = "";
 };
 int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* p);
@@ -94,6 +95,6 @@ int zm_launch_pair(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, cons
 // diagonal (n) -> ghost-padded [nz][ny+4][nx+4]
 int zm_pad_diag(const sdb_matrix* m, double* padded, cudaStream_t s);
 // probes (n x ldv) -> padded block
-int zm_pad(const sdb_matrix* m, const double* probes, int64_t ldv, double* padded, cudaStream_t s);
+int zm_pad(const sdb_matrix* m, const ZmPlan& p, const double* probes, int64_t ldv, double* padded, cudaStream_t s);
 
 }  // namespace sdb

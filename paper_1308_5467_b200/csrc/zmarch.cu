@@ -48,6 +48,7 @@ struct ZmArgs {
   int slices;                 // ldv / CS
   int R;                      // ring slots
   int64_t items;              // n_xt * n_yt * n_zs * slices
+  int G;                      // ghost width of the padded blocks (1, or 2 with fused pairs)
   const double* diag;         // n (unpadded)
   double wc[27];              // weights, lexicographic (dz, dy, dx); centre unused
 };
@@ -121,17 +122,18 @@ struct ZmGeom {
   static_assert(NT % 32 == 0 && NT <= 1024 - 32, "consumer threads");
 };
 
-// Ghost width of the padded blocks [nz][ny+2G][nx+2G][ldv]: 2, so the fused
-// two-step kernel's halo-2 boxes are single TMA rectangles too.
+// Ghost width of the padded blocks [nz][ny+2G][nx+2G][ldv]: 1 for single
+// steps, 2 when fused pairs run (their halo-2 boxes are single TMA
+// rectangles too); the fused kernel is compiled for kZmGhost.
 constexpr int kZmGhost = 2;
 
 // Store w at padded offset dst of point (x, y) and at every periodic ghost
 // image of it (x within G of an x face, y of a y face, and the corner).
 __device__ __forceinline__ void zm_store_ghosted(double* dst, double2 w, int x, int y, int nx, int ny, int64_t ldv,
-                                                 int64_t pstride_y) {
+                                                 int64_t pstride_y, int G) {
   st_d2_cs(dst, w);
-  const int gx = x < kZmGhost ? nx : (x >= nx - kZmGhost ? -nx : 0);
-  const int gy = y < kZmGhost ? ny : (y >= ny - kZmGhost ? -ny : 0);
+  const int gx = x < G ? nx : (x >= nx - G ? -nx : 0);
+  const int gy = y < G ? ny : (y >= ny - G ? -ny : 0);
   if (gx) st_d2_cs(dst + (int64_t)gx * ldv, w);
   if (gy) st_d2_cs(dst + (int64_t)gy * pstride_y, w);
   if (gx && gy) st_d2_cs(dst + (int64_t)gx * ldv + (int64_t)gy * pstride_y, w);
@@ -180,8 +182,8 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
   __syncthreads();
 
   const int nx = t.nx, ny = t.ny, nz = t.nz;
-  const int64_t pstride_y = (int64_t)(nx + 2 * kZmGhost) * a.ldv;  // padded row of points
-  const int64_t pplane = (int64_t)(ny + 2 * kZmGhost) * pstride_y;  // padded plane
+  const int64_t pstride_y = (int64_t)(nx + 2 * t.G) * a.ldv;  // padded row of points
+  const int64_t pplane = (int64_t)(ny + 2 * t.G) * pstride_y;  // padded plane
   const int64_t G_ = gridDim.x;
 
   if (tid >= NT) {
@@ -205,10 +207,10 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
           const bool outp = p >= zbeg && p < zend;
           double* slot = zsm + (int64_t)s * SL::DOUBLES;
           mbar_expect_tx(full + s, outp ? SL::FULL_BYTES : SL::HALO_BYTES);
-          tma_load_4d(slot + SL::X0, &maps.x, full + s, c0, x0 + kZmGhost - 1, y0 + kZmGhost - 1, zw);
+          tma_load_4d(slot + SL::X0, &maps.x, full + s, c0, x0 + t.G - 1, y0 + t.G - 1, zw);
           if (outp) {
-            if (SL::PB) tma_load_4d(slot + SL::P0, &maps.prev, full + s, c0, x0 + kZmGhost, y0 + kZmGhost, p);
-            if (SL::VB) tma_load_4d(slot + SL::V0, &maps.v0, full + s, c0, x0 + kZmGhost, y0 + kZmGhost, p);
+            if (SL::PB) tma_load_4d(slot + SL::P0, &maps.prev, full + s, c0, x0 + t.G, y0 + t.G, p);
+            if (SL::VB) tma_load_4d(slot + SL::V0, &maps.v0, full + s, c0, x0 + t.G, y0 + t.G, p);
             tma_load_3d(slot + SL::D0, &maps.diag, full + s, x0, y0, p);
           }
           if (++s == t.R) {
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
       xo[k] = ((py + 1) * (TX + 2) + (px + 1)) * CS + 2 * q;  // centre in the x halo box
       io[k] = (py * TX + px) * CS + 2 * q;                    // in the interior boxes
       dio[k] = py * TX + px;                                  // in the diagonal box
-      cofs[k] = (int64_t)zbeg * pplane + (int64_t)(cy[k] + kZmGhost) * pstride_y + (int64_t)(cx[k] + kZmGhost) * a.ldv + col0 +
+      cofs[k] = (int64_t)zbeg * pplane + (int64_t)(cy[k] + t.G) * pstride_y + (int64_t)(cx[k] + t.G) * a.ldv + col0 +
                 2 * q;
     }
     // rolling accumulators: at plane p, accC = out(p), accN = out(p+1), accP = out(p-1)
@@ -306,7 +308,7 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
           }
           double* dst = pn + cofs[k];
           st_d2_cs(dst, wn);
-          zm_store_ghosted(dst, wn, cx[k], cy[k], nx, ny, a.ldv, pstride_y);
+          zm_store_ghosted(dst, wn, cx[k], cy[k], nx, ny, a.ldv, pstride_y, t.G);
           if (MODE == SDB_CHEB_DOUBLING) {
             accA.x += wn.x * wn.x;
             accA.y += wn.y * wn.y;
@@ -561,7 +563,7 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
           *reinterpret_cast<double2*>(w1 + e1[k] * CS + 2 * q) = wn;
           if (own_plane && own1[k]) {
             zm_store_ghosted(a.next + (int64_t)q1 * pplane + gofs1[k], wn, x0 + ex - 1, y0 + ey - 1, nx, ny, a.ldv,
-                             pstride_y);
+                             pstride_y, kZmGhost);
             accA1.x += wn.x * wn.x;
             accA1.y += wn.y * wn.y;
             accB1.x += wn.x * xi.x;
@@ -620,7 +622,7 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
             const double ty = (a2P[k].y - a.c * wi.y) * a.inv_d;
             const double2 wn = make_double2(2.0 * tx - xk.x, 2.0 * ty - xk.y);
             zm_store_ghosted(a.next2 + (int64_t)q2 * pplane + gofs2[k], wn, x0 + ex - 1, y0 + ey - 1, nx, ny, a.ldv,
-                             pstride_y);
+                             pstride_y, kZmGhost);
             accA2.x += wn.x * wn.x;
             accA2.y += wn.y * wn.y;
             accB2.x += wn.x * wi.x;
@@ -675,6 +677,7 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
 
 // diagonal (n) -> ghost-padded [nz][ny+2G][nx+2G]
 __global__ void zm_pad_diag_kernel(const double* __restrict__ src, int nx, int ny, int nz, double* __restrict__ dst) {
+  // (fused pairs only: ghost width kZmGhost)
   const int px = nx + 2 * kZmGhost, py = ny + 2 * kZmGhost;
   const int64_t total = (int64_t)nz * py * px;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -691,19 +694,19 @@ __global__ void zm_pad_diag_kernel(const double* __restrict__ src, int nx, int n
 }
 
 // Probe block (n x ldv) -> ghost-padded block [nz][ny+2G][nx+2G][ldv].
-__global__ void zm_pad_kernel(const double* __restrict__ src, int nx, int ny, int nz, int64_t ldv,
+__global__ void zm_pad_kernel(const double* __restrict__ src, int nx, int ny, int nz, int64_t ldv, int G,
                               double* __restrict__ dst) {
-  const int64_t pts = (int64_t)nz * (ny + 2 * kZmGhost) * (nx + 2 * kZmGhost);
+  const int64_t pts = (int64_t)nz * (ny + 2 * G) * (nx + 2 * G);
   const int64_t h = ldv / 2;  // double2 per point
   const int64_t total = pts * h;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = i % h, pt = i / h;
-    const int xx = (int)(pt % (nx + 2 * kZmGhost));
-    const int64_t r = pt / (nx + 2 * kZmGhost);
-    const int yy = (int)(r % (ny + 2 * kZmGhost));
-    const int z = (int)(r / (ny + 2 * kZmGhost));
-    int x = xx - kZmGhost, y = yy - kZmGhost;
+    const int xx = (int)(pt % (nx + 2 * G));
+    const int64_t r = pt / (nx + 2 * G);
+    const int yy = (int)(r % (ny + 2 * G));
+    const int z = (int)(r / (ny + 2 * G));
+    int x = xx - G, y = yy - G;
     x = x < 0 ? x + nx : (x >= nx ? x - nx : x);
     y = y < 0 ? y + ny : (y >= ny ? y - ny : y);
     const int64_t s = (((int64_t)z * ny + y) * nx + x) * ldv + 2 * c;
@@ -877,8 +880,6 @@ int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* out) {
   if (best_g > p.items) best_g = p.items;
   p.grid = best_g;
   p.nbp = p.grid / slices;
-  p.block_bytes = sizeof(double) * (size_t)nz * (ny + 2 * kZmGhost) * (nx + 2 * kZmGhost) * (size_t)ldv;
-  p.block_bytes = (p.block_bytes + 255) & ~(size_t)255;
   p.name = "cheb_step_zmarch";
   // fused pairs of steps (doubling mode, opt-in with SDB_ZM_FUSE=1): measured
   // 1.8-2.6x SLOWER per step than single steps on C2/C5 (profiles/
@@ -900,6 +901,9 @@ int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* out) {
       p.name = "cheb_step2_zmarch";
     }
   }
+  p.G = p.fuse ? kZmGhost : 1;
+  p.block_bytes = sizeof(double) * (size_t)nz * (ny + 2 * p.G) * (nx + 2 * p.G) * (size_t)ldv;
+  p.block_bytes = (p.block_bytes + 255) & ~(size_t)255;
   p.on = true;
   *out = p;
   return SDB_OK;
@@ -925,7 +929,7 @@ int zm_launch_step(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, bool
   const ZmCfg c = kZmCfgs[p.cfg];
   ZmMaps maps;
   auto encode = [&](CUtensorMap* map, const double* base, int bx, int by) -> int {
-    const int px = nx + 2 * kZmGhost, py = ny + 2 * kZmGhost;
+    const int px = nx + 2 * p.G, py = ny + 2 * p.G;
     cuuint64_t gdim[4] = {(cuuint64_t)a.ldv, (cuuint64_t)px, (cuuint64_t)py, (cuuint64_t)nz};
     cuuint64_t gstr[3] = {(cuuint64_t)a.ldv * 8, (cuuint64_t)px * a.ldv * 8, (cuuint64_t)py * px * a.ldv * 8};
     cuuint32_t box[4] = {(cuuint32_t)c.CS, (cuuint32_t)bx, (cuuint32_t)by, 1};
@@ -960,6 +964,7 @@ int zm_launch_step(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, bool
   t.slices = (int)(a.ldv / c.CS);
   t.R = p.R;
   t.items = p.items;
+  t.G = p.G;
   t.diag = m->diag;
   for (int o = 0; o < 27; ++o) t.wc[o] = o < m->nterms ? m->term_w_host[o] : 0.0;
   StepArgs aa = a;
@@ -1045,13 +1050,13 @@ int zm_pad_diag(const sdb_matrix* m, double* padded, cudaStream_t s) {
   return SDB_OK;
 }
 
-int zm_pad(const sdb_matrix* m, const double* probes, int64_t ldv, double* padded, cudaStream_t s) {
+int zm_pad(const sdb_matrix* m, const ZmPlan& p, const double* probes, int64_t ldv, double* padded, cudaStream_t s) {
   const int nx = (int)m->st.nx, ny = (int)m->st.ny, nz = (int)m->st.nz;
-  const int64_t total = (int64_t)nz * (ny + 2 * kZmGhost) * (nx + 2 * kZmGhost) * (ldv / 2);
+  const int64_t total = (int64_t)nz * (ny + 2 * p.G) * (nx + 2 * p.G) * (ldv / 2);
   int64_t blocks = (total + 255) / 256;
   const int64_t cap = 8LL * num_sms(m->device);
   if (blocks > cap) blocks = cap;
-  zm_pad_kernel<<<(unsigned)blocks, 256, 0, s>>>(probes, nx, ny, nz, ldv, padded);
+  zm_pad_kernel<<<(unsigned)blocks, 256, 0, s>>>(probes, nx, ny, nz, ldv, p.G, padded);
   SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
