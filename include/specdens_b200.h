@@ -234,6 +234,17 @@ SDB_API int sdb_ritz_residual_bounds(const double* alpha, const double* beta, co
 SDB_API int sdb_haydock(const double* alpha, const double* beta, const int32_t* steps_done,
                 const int32_t* status, int64_t n_vec, int64_t m, const double* grid, int64_t n_pts,
                 double eta, double* density, double* trunc_pts, double* trunc, void* stream);
+/* Delta-Gauss-Legendre (dgl.py:42-132), one expansion centre t_i per thread:
+ * gamma_k(t_i) by the erf-seeded recurrence with psi_k partial sums, halted at
+ * the first k >= 1 with |gamma_{k-1}| + |gamma_k| <= k tol (effective[i] = k;
+ * later gammas are 0).  values[i] = sum_k weights[k] gamma_k(t_i) / divisor
+ * (weights = (k + 1/2) zeta_k; values/weights may be NULL); gamma, psi
+ * ((degree+1) x n_pts row-major) and effective (int32 n_pts) are optional
+ * device outputs; *failed (device int32, caller-zeroed) gets the first
+ * non-finite step.  sigma in unit coordinates. */
+SDB_API int sdb_dgl(const double* weights, int64_t degree, const double* t, int64_t n_pts, double sigma,
+            double tol, double divisor, double* values, double* gamma, double* psi, int32_t* effective,
+            int32_t* failed, void* stream);
 /* continued_fraction_resolvent / tridiagonal_resolvent_first (lanczos.py:222-260)
  * for one tridiagonal (alpha m, beta m-1) at nz complex points z (interleaved
  * re, im); outputs interleaved complex, each may be NULL.  scratch: 4*m*nz

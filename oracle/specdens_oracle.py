@@ -403,3 +403,49 @@ def haydock_dos(matrix, steps, kind, seed, n_vec, eta, grid, reorth="full"):
         dens.append(-np.imag(f) / np.pi)
         trunc.append(bn * float(np.max(np.abs(w_last))))
     return np.mean(dens, axis=0), max(trunc)
+
+
+# ---- dgl.py:35-132 (Delta-Gauss-Legendre) ---------------------------------------------------------
+def dgl_gamma_table(t, sigma, max_degree, tol=1e-6):
+    """(gamma, psi, effective) for centres t (dgl.py:42-89)."""
+    from scipy.special import erf
+
+    t = np.asarray(t, dtype=float)
+    gamma = np.zeros((max_degree + 1, t.size))
+    psi = np.zeros((max_degree + 1, t.size))
+    s = np.sqrt(2.0) * sigma
+    gamma[0] = sigma * np.sqrt(np.pi / 2.0) * (erf((1.0 - t) / s) + erf((1.0 + t) / s))
+    effective = np.full(t.size, max_degree)
+    active = np.ones(t.size, dtype=bool)
+    exp_lo = np.exp(-0.5 * ((1.0 - t) / sigma) ** 2)
+    exp_hi = np.exp(-0.5 * ((1.0 + t) / sigma) ** 2)
+    psi_k = np.zeros(t.size)
+    psi_next = gamma[0].copy()
+    if max_degree >= 1:
+        psi[1] = psi_next
+    for k in range(max_degree):
+        if k >= 1:
+            halted = active & (np.abs(gamma[k - 1]) + np.abs(gamma[k]) <= k * tol)
+            effective[halted] = k
+            active &= ~halted
+            if not active.any():
+                break
+        boundary_term = exp_lo - (-1.0) ** k * exp_hi
+        gamma_prev = gamma[k - 1] if k >= 1 else 0.0
+        nxt = ((2 * k + 1) / (k + 1.0) * (sigma * sigma * (psi_k - boundary_term) + t * gamma[k])
+               - k / (k + 1.0) * gamma_prev)
+        gamma[k + 1, active] = nxt[active]
+        j = k + 1
+        psi_k, psi_next = psi_next, (2 * j + 1) * gamma[j] + psi_k
+        if j + 1 <= max_degree:
+            psi[j + 1, active] = psi_next[active]
+    return gamma, psi, effective
+
+
+def dgl_dos(zeta, n, d, sigma, t, tol=1e-6):
+    """(values, density) of evaluate_dgl_dos (dgl.py:109-132); sigma in original units."""
+    sigma_m = sigma / d
+    gamma, _, _ = dgl_gamma_table(t, sigma_m, len(zeta) - 1, tol)
+    k = np.arange(len(zeta))
+    values = (((k + 0.5) * zeta) @ gamma) / (n * np.sqrt(2.0 * np.pi) * sigma_m)
+    return values, values / d

@@ -6,10 +6,12 @@ probe mean, finiteness check, coefficients, Clenshaw, 1/sqrt(1-t^2) and the
 1/d unmapping -- stays on the device and the host reads back the moments and
 the density once.  The moment-sharing variants ``spectroscopic``,
 ``delta-cheb`` (same Chebyshev moments) and ``kpml`` (Legendre moments from
-the same fused kernels) run through the same kernels.  ``haydock``
-evaluates the same batched Lanczos tridiagonals' resolvents on the device
-(§8(f)-3).  The remaining reference methods (dgl, cdos) are outside the
-accelerated path and raise ``NotImplementedError``.
+the same fused kernels) run through the same kernels.  ``dgl``
+runs its gamma recurrence on the same Legendre moments, and ``haydock``
+evaluates the batched Lanczos tridiagonals' resolvents on the device
+(§8(f)-3).  The remaining reference method (cdos, a monotone-spline
+refinement of the Lanczos staircase) is outside the accelerated path and
+raises ``NotImplementedError``.
 """
 
 import time
@@ -21,6 +23,7 @@ from . import engine as E
 from . import kpm as K
 from .density import DEFAULT_GRID_POINTS, SpectralDensityEstimate, interval_grid, unit_grid
 from .errors import NumericalFailure
+from .dgl import evaluate_dgl_dos
 from .lanczos import haydock_dos, lanczos_dos
 from .operators import MatvecCounter, apply_spectral_map, as_operator
 
@@ -28,7 +31,7 @@ CHEBYSHEV_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb")
 LEGENDRE_METHODS = ("kpml", "dgl")
 LANCZOS_METHODS = ("lanczos", "haydock", "cdos")
 ALL_METHODS = CHEBYSHEV_METHODS + LEGENDRE_METHODS + LANCZOS_METHODS
-GPU_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb", "kpml", "lanczos", "haydock")
+GPU_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb", "kpml", "dgl", "lanczos", "haydock")
 
 
 def analytic_matvec_count(method, degree, n_vec, product_formula=False):
@@ -104,10 +107,13 @@ def estimate_dos(matrix, interval, method, degree, source, n_vec, sigma=None, et
             est = K.spectroscopic_dos(moments, interval, grid, device=device)
         else:
             est = K.delta_chebyshev_dos(moments, interval, grid, device=device)
-    elif method == "kpml":
+    elif method in LEGENDRE_METHODS:
         mapped = apply_spectral_map(counter, interval)
         moments = K.compute_legendre_moments(mapped, degree, source, n_vec, threads, device=device)
-        est = K.evaluate_kpml_dos(moments, interval, unit_grid(grid_points), device=device)
+        if method == "kpml":
+            est = K.evaluate_kpml_dos(moments, interval, unit_grid(grid_points), device=device)
+        else:
+            est = evaluate_dgl_dos(moments, interval, sigma, unit_grid(grid_points), device=device)
     else:
         grid = interval_grid(interval, grid_points)
         if method == "lanczos":

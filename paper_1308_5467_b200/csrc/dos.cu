@@ -346,6 +346,67 @@ __global__ void max_reduce_kernel(const double* __restrict__ x, int64_t n, doubl
   if (threadIdx.x == 0) *out = red[0];
 }
 
+// ---- Delta-Gauss-Legendre (dgl.py:42-132) -------------------------------------------
+// One expansion centre per thread: the gamma_k / psi_k recurrence seeded by the
+// erf formula, halted at the first k >= 1 with |gamma_{k-1}| + |gamma_k| <= k tol
+// (later gammas are zero), accumulating sum_k w_k gamma_k with w_k =
+// (k + 1/2) zeta_k when w is given.  gamma/psi tables ((M+1) x n_pts,
+// row-major) are optional outputs (compute_dgl_coefficients).
+__global__ void dgl_kernel(const double* __restrict__ w, int64_t degree, const double* __restrict__ t, int64_t n_pts,
+                           double sigma, double tol, double divisor, double* __restrict__ values,
+                           double* __restrict__ gamma_out, double* __restrict__ psi_out, int32_t* __restrict__ eff,
+                           int32_t* failed) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_pts) return;
+  const double ti = t[i];
+  const double s2 = sqrt(2.0) * sigma;
+  const double g0 = sigma * sqrt(M_PI / 2.0) * (erf((1.0 - ti) / s2) + erf((1.0 + ti) / s2));
+  const double exp_lo = exp(-0.5 * ((1.0 - ti) / sigma) * ((1.0 - ti) / sigma));
+  const double exp_hi = exp(-0.5 * ((1.0 + ti) / sigma) * ((1.0 + ti) / sigma));
+  double gk = g0, gprev = 0.0;           // gamma_k, gamma_{k-1}
+  double psi_k = 0.0, psi_next = g0;     // psi_k, psi_{k+1}
+  double acc = w ? w[0] * g0 : 0.0;
+  int64_t effective = degree;
+  if (gamma_out) {
+    for (int64_t k = 0; k <= degree; ++k) {
+      gamma_out[k * n_pts + i] = 0.0;
+      if (psi_out) psi_out[k * n_pts + i] = 0.0;
+    }
+    gamma_out[i] = g0;
+    if (psi_out && degree >= 1) psi_out[n_pts + i] = psi_next;
+  }
+  for (int64_t k = 0; k < degree; ++k) {
+    if (k >= 1 && fabs(gprev) + fabs(gk) <= (double)k * tol) {
+      effective = k;
+      break;
+    }
+    // NumPy's operation order with no FMA contraction: the recurrence
+    // amplifies rounding differences once the gammas have decayed
+    const double boundary = __dsub_rn(exp_lo, __dmul_rn((k & 1) ? -1.0 : 1.0, exp_hi));
+    const double inner = __dadd_rn(__dmul_rn(__dmul_rn(sigma, sigma), __dsub_rn(psi_k, boundary)), __dmul_rn(ti, gk));
+    const double nxt = __dsub_rn(__dmul_rn((double)(2 * k + 1) / ((double)k + 1.0), inner),
+                                 __dmul_rn((double)k / ((double)k + 1.0), gprev));
+    if (!isfinite(nxt)) {
+      atomicExch(failed, (int32_t)(k + 1));
+      effective = k;
+      break;
+    }
+    gprev = gk;
+    gk = nxt;
+    const int64_t j = k + 1;
+    if (w) acc = __dadd_rn(acc, __dmul_rn(w[j], gk));
+    const double pn = __dadd_rn(__dmul_rn((double)(2 * j + 1), gk), psi_k);
+    psi_k = psi_next;
+    psi_next = pn;
+    if (gamma_out) {
+      gamma_out[j * n_pts + i] = gk;
+      if (psi_out && j + 1 <= degree) psi_out[(j + 1) * n_pts + i] = psi_next;
+    }
+  }
+  if (values) values[i] = acc / divisor;
+  if (eff) eff[i] = (int32_t)effective;
+}
+
 // ---- node pooling (lanczos.py:170-177) ---------------------------------------------
 // Stable rank sort of the concatenated nodes: rank(i) = #{j : th_j < th_i} +
 // #{j < i : th_j == th_i}.  O(N^2) compares on a tile of theta staged in
@@ -486,6 +547,21 @@ int sdb_haydock(const double* alpha, const double* beta, const int32_t* steps_do
     max_reduce_kernel<<<1, 256, 0, s>>>(trunc_pts, n_pts, trunc);
     SDB_CHECK_LAUNCH();
   }
+  return SDB_OK;
+}
+
+int sdb_dgl(const double* weights, int64_t degree, const double* t, int64_t n_pts, double sigma, double tol,
+            double divisor, double* values, double* gamma, double* psi, int32_t* effective, int32_t* failed,
+            void* stream) {
+  SDB_REQUIRE(t && failed, "NULL argument");
+  SDB_REQUIRE(degree >= 0, "max degree must be non-negative");
+  SDB_REQUIRE(sigma > 0.0, "sigma must be positive");
+  SDB_REQUIRE(tol > 0.0, "tol must be positive");
+  SDB_REQUIRE(values == nullptr || weights != nullptr, "values need the weights");
+  if (n_pts <= 0) return SDB_OK;
+  dgl_kernel<<<(unsigned)((n_pts + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      weights, degree, t, n_pts, sigma, tol, divisor, values, gamma, psi, effective, failed);
+  SDB_CHECK_LAUNCH();
   return SDB_OK;
 }
 

@@ -146,6 +146,21 @@ def variants_case(name, op, kind, n_vec, degree, n_pts):
         est = estimate_dos(mat, iv, method, degree, src, n_vec, grid_points=n_pts)
         out[f"estimate_{method}_density"] = est.density
         out[f"estimate_{method}_matvec_count"] = est.params["matvec_count"]
+    from specdens.dgl import compute_dgl_coefficients, evaluate_dgl_dos
+    sigma = 0.05 * iv.halfwidth
+    dgl = evaluate_dgl_dos(leg, iv, sigma, grid)
+    out["dgl_sigma"] = sigma
+    out["dgl_density"] = dgl.density
+    out["dgl_effective_degree"] = dgl.params["effective_degree"]
+    est = estimate_dos(mat, iv, "dgl", degree, src, n_vec, sigma=sigma, grid_points=n_pts)
+    out["estimate_dgl_density"] = est.density
+    out["estimate_dgl_matvec_count"] = est.params["matvec_count"]
+    for i, tc in enumerate((-0.9, -0.3, 0.0, 0.55)):
+        co = compute_dgl_coefficients(tc, 0.05, degree)
+        out[f"dglcoef{i}_t"] = tc
+        out[f"dglcoef{i}_gamma"] = co.gamma
+        out[f"dglcoef{i}_psi"] = co.psi
+        out[f"dglcoef{i}_effective"] = co.effective_degree
     print(f"{name}: n={mat.dim} {time.time() - t0:.1f}s", flush=True)
     return out
 

@@ -127,6 +127,21 @@ def _variants(golden, name, op):
         est = sdb.estimate_dos(op, iv, method, degree, src, n_vec, grid_points=n_pts)
         assert np.max(np.abs(est.density - g[f"estimate_{method}_density"])) <= DOS_ATOL, method
         assert est.params["matvec_count"] == int(g[f"estimate_{method}_matvec_count"])
+    # Delta-Gauss-Legendre on the same Legendre moments (dgl.py:109-132)
+    sigma = float(g["dgl_sigma"])
+    dgl = sdb.evaluate_dgl_dos(leg, iv, sigma, grid)
+    assert np.max(np.abs(dgl.density - g["dgl_density"])) <= DOS_ATOL
+    assert dgl.params["effective_degree"] == int(g["dgl_effective_degree"])
+    est = sdb.estimate_dos(op, iv, "dgl", degree, src, n_vec, sigma=sigma, grid_points=n_pts)
+    assert np.max(np.abs(est.density - g["estimate_dgl_density"])) <= DOS_ATOL
+    assert est.params["matvec_count"] == int(g["estimate_dgl_matvec_count"])
+    for i in range(4):
+        co = sdb.compute_dgl_coefficients(float(g[f"dglcoef{i}_t"]), 0.05, degree)
+        assert co.effective_degree == int(g[f"dglcoef{i}_effective"])
+        np.testing.assert_allclose(co.gamma, g[f"dglcoef{i}_gamma"], rtol=0, atol=1e-12)
+        psi_ref = g[f"dglcoef{i}_psi"]
+        # psi is a running sum of an unstable recurrence: erf/exp ulps grow towards the cutoff
+        assert np.max(np.abs(co.psi - psi_ref)) <= 1e-10 * np.max(np.abs(psi_ref))
 
 
 def test_variants_c1_csr(golden):
@@ -146,3 +161,24 @@ def test_variants_c5small_stencil_kernels(golden, monkeypatch, zmarch):
     # the CSR form of the same operator (stencil detection off -> CSR kernel)
     monkeypatch.setenv("SDB_AUTO_STENCIL", "0")
     _variants(golden, "variants_c5small", sdb.SparseSymmetricMatrix(csr=op.csr))
+
+
+def test_dgl_contract():
+    """dgl.py contract: argument checks, gamma_0 closed form, kernel halting."""
+    with pytest.raises(ValueError):
+        sdb.compute_dgl_coefficients(1.0, 0.1, 10)
+    with pytest.raises(ValueError):
+        sdb.compute_dgl_coefficients(0.0, 0.0, 10)
+    with pytest.raises(ValueError):
+        sdb.compute_dgl_coefficients(0.0, 0.1, 10, tol=0.0)
+    co = sdb.compute_dgl_coefficients(0.2, 0.1, 200)
+    assert co.gamma[0] == pytest.approx(float(sdb.gamma_zero(0.2, 0.1)), rel=1e-14)
+    assert 1 <= co.effective_degree <= 200 and len(co.gamma) == co.effective_degree + 1
+    m = sdb.MomentSequence(zeta=np.ones(3), degree=2, n_vec=1, basis="chebyshev", n=1)
+    with pytest.raises(ValueError):
+        sdb.evaluate_dgl_dos(m, UNIT, 0.1)
+    leg = sdb.MomentSequence(zeta=np.ones(3), degree=2, n_vec=1, basis="legendre", n=1)
+    with pytest.raises(ValueError):
+        sdb.evaluate_dgl_dos(leg, UNIT, 0.1, grid=np.array([1.0]))
+    with pytest.raises(ValueError):
+        sdb.evaluate_dgl_dos(leg, UNIT, -0.1)

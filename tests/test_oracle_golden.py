@@ -115,6 +115,14 @@ def test_oracle_variants_match_reference(golden, name):
     np.testing.assert_array_equal(cheb, g["zeta_chebyshev"])
     np.testing.assert_array_equal(O.spectroscopic_dos(cheb, n, d, t)[1], g["spectroscopic_density"])
     np.testing.assert_array_equal(O.delta_chebyshev_dos(cheb, n, d, t, g["delta_degrees"])[1], g["delta_density"])
+    # Delta-Gauss-Legendre (dgl.py:42-132)
+    np.testing.assert_array_equal(O.dgl_dos(leg, n, d, float(g["dgl_sigma"]), t)[1], g["dgl_density"])
+    for i in range(4):
+        ga, ps, ef = O.dgl_gamma_table(np.array([float(g[f"dglcoef{i}_t"])]), 0.05, degree)
+        k = int(ef[0])
+        assert k == int(g[f"dglcoef{i}_effective"])
+        np.testing.assert_array_equal(ga[: k + 1, 0], g[f"dglcoef{i}_gamma"])
+        np.testing.assert_array_equal(ps[: k + 1, 0], g[f"dglcoef{i}_psi"])
 
 
 def _interval_matrices(g):
