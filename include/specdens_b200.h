@@ -172,6 +172,19 @@ SDB_API int sdb_cheb_partials_size(const sdb_matrix* m, int64_t n_vec, int64_t d
 SDB_API int sdb_cheb_step(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode,
                   int64_t k, const double* x, const double* prev, double* next, const double* v0,
                   double* partials, size_t partial_bytes, void* stream);
+/* sdb_cheb_step for a z-slab stencil handle (row partition) that also pushes
+ * the halo: the first own plane of `next` is stored to halo_lo (the lower
+ * neighbour slab's upper ghost plane, nx*ny x ldv), the last own plane to
+ * halo_hi (the upper neighbour's lower ghost plane), from the same kernel
+ * epilogue that stores them locally -- peer-device memory over NVLink (P2P
+ * enabled, sdb_enable_peer_access) or this device; either may be NULL.  The
+ * caller orders step k+1 after the neighbours' step k (same stream, or events). */
+SDB_API int sdb_cheb_step_halo(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode,
+                       int64_t k, const double* x, const double* prev, double* next, const double* v0,
+                       double* partials, size_t partial_bytes, double* halo_lo, double* halo_hi, void* stream);
+/* cudaDeviceEnablePeerAccess(peer) from `device` (already-enabled is success);
+ * returns SDB_EUNSUPPORTED if the pair cannot access each other. */
+SDB_API int sdb_enable_peer_access(int device, int peer);
 SDB_API int sdb_cheb_reduce(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode, const double* partials,
                     double* zeta_pp, void* stream);
 /* zeta[k] = (1/n_vec) sum_l zeta_pp[l][k], probes summed in index order

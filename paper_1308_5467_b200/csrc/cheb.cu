@@ -89,6 +89,7 @@ __device__ __forceinline__ void epi_finish(const StepArgs& a, int64_t row, int q
       wn.y = 2.0 * ty - e.wp[v].y;
     }
     st_d2_once(a.next + o + 2 * L * v, wn, pol);
+    halo_push(a, row, 2 * q + 2 * L * v, wn);
     if (MODE == SDB_CHEB_DOUBLING) {
       accA[v].x += wn.x * wn.x;
       accA[v].y += wn.y * wn.y;
@@ -290,6 +291,8 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
   a.prev += slice * cs;
   a.next += slice * cs;
   a.v0 += slice * cs;
+  if (a.halo_lo) a.halo_lo += slice * cs;
+  if (a.halo_hi) a.halo_hi += slice * cs;
   constexpr int RPW = 32 / L;
   constexpr int RPB = RPW * kStepWarps;
   constexpr int U = VPL == 1 ? SDB_U_V1 : 2;
@@ -911,9 +914,28 @@ int sdb_cheb_partials_size(const sdb_matrix* m, int64_t n_vec, int64_t degree, i
   return SDB_OK;
 }
 
+static int cheb_step_impl(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode,
+                          int64_t k, const double* x, const double* prev, double* next, const double* v0,
+                          double* partials, size_t partial_bytes, double* halo_lo, double* halo_hi, void* stream);
+
 int sdb_cheb_step(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode, int64_t k,
                   const double* x, const double* prev, double* next, const double* v0, double* partials,
                   size_t partial_bytes, void* stream) {
+  return cheb_step_impl(m, c, d, n_vec, degree, mode, k, x, prev, next, v0, partials, partial_bytes, nullptr,
+                        nullptr, stream);
+}
+
+int sdb_cheb_step_halo(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode, int64_t k,
+                       const double* x, const double* prev, double* next, const double* v0, double* partials,
+                       size_t partial_bytes, double* halo_lo, double* halo_hi, void* stream) {
+  SDB_REQUIRE(m && m->format == SDB_FMT_STENCIL, "halo push needs a stencil slab handle");
+  return cheb_step_impl(m, c, d, n_vec, degree, mode, k, x, prev, next, v0, partials, partial_bytes, halo_lo,
+                        halo_hi, stream);
+}
+
+static int cheb_step_impl(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode,
+                          int64_t k, const double* x, const double* prev, double* next, const double* v0,
+                          double* partials, size_t partial_bytes, double* halo_lo, double* halo_hi, void* stream) {
   SDB_REQUIRE(m && x && partials, "NULL argument");
   int legendre;
   mode = split_mode(mode, &legendre);
@@ -933,6 +955,12 @@ int sdb_cheb_step(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_
   StepPlan P;
   if ((rc = plan_steps(m, n_vec, mode, c, d, &P))) return rc;
   P.a.legendre = legendre;
+  if (halo_lo || halo_hi) {
+    P.a.halo_lo = halo_lo;
+    P.a.halo_hi = halo_hi;
+    P.a.halo_rows = m->st.nx * m->st.ny;
+    P.a.last_row0 = (m->st.nz - 1) * P.a.halo_rows;
+  }
   return launch_plan_step(m, P, degree, mode, k, x, prev, next, v0 ? v0 : x, partials, (cudaStream_t)stream);
 }
 

@@ -418,3 +418,19 @@ int sdb_unpack_block(const double* block, int64_t n, int64_t ldv, int64_t n_vec,
 }
 
 }  // extern "C"
+
+extern "C" int sdb_enable_peer_access(int device, int peer) {
+  if (device == peer) return SDB_OK;
+  int can = 0;
+  SDB_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+  if (!can) return sdb::fail(SDB_EUNSUPPORTED, "device %d cannot access peer %d", device, peer);
+  sdb::DeviceGuard dg(device);
+  if (!dg.ok) return sdb::fail(SDB_ECUDA, "cannot select CUDA device %d", device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    (void)cudaGetLastError();
+    return SDB_OK;
+  }
+  if (e != cudaSuccess) return sdb::cuda_fail(e, "cudaDeviceEnablePeerAccess", __FILE__, __LINE__);
+  return SDB_OK;
+}

@@ -25,6 +25,13 @@ struct StepArgs {
   // w_{k+1} = (la t - lb w_{k-1}) / lc with la = 2k+1, lb = k, lc = k+1
   int legendre;
   double la, lb, lc;
+  // row partition (z-slabs): the step also stores its first / last own plane
+  // of w_{k+1} into the neighbouring slabs' ghost planes (peer memory over
+  // NVLink, or the same device); NULL: no push
+  double* halo_lo;     // lower neighbour's upper ghost plane (nxy x ldv)
+  double* halo_hi;     // upper neighbour's lower ghost plane
+  int64_t halo_rows;   // rows per plane (nx*ny)
+  int64_t last_row0;   // first row of the last own plane
   // fused two-step z-march (zmarch.cu): w_{k+2} and its moment slots
   double* next2;
   int slotA2;          // <w++,w++>  (-1: none)
@@ -36,6 +43,14 @@ inline int split_mode(int mode, int* legendre) {
   *legendre = mode == SDB_LEGENDRE;
   return mode == SDB_LEGENDRE ? SDB_CHEB_DIRECT : mode;
 }
+// Halo push of one stored double2 (row-local offset o = row*ldv + column).
+__device__ __forceinline__ void halo_push(const StepArgs& a, int64_t row, int64_t col_ofs, double2 w) {
+  if (a.halo_lo && row < a.halo_rows)
+    *reinterpret_cast<double2*>(a.halo_lo + row * a.ldv + col_ofs) = w;
+  if (a.halo_hi && row >= a.last_row0)
+    *reinterpret_cast<double2*>(a.halo_hi + (row - a.last_row0) * a.ldv + col_ofs) = w;
+}
+
 inline void set_step_scalars(StepArgs& a, int64_t k) {
   a.la = (double)(2 * k + 1);
   a.lb = (double)k;

@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, St
       }
       const int64_t row = (int64_t)z * plane_rows + (y0 + iy) * nx + (x0 + ix);
       st_d2_once(a.next + row * a.ldv + col0 + 2 * q, wn, pol);
+      halo_push(a, row, col0 + 2 * q, wn);
       accA.x += wn.x * wn.x;
       accA.y += wn.y * wn.y;
       accB.x += wn.x * xi.x;

@@ -21,6 +21,7 @@ callables so the same driver runs the CUDA path (``DeviceSlab``) and a CPU
 reference slab in the multi-process gloo tests.
 """
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -109,7 +110,9 @@ class DeviceSlab:
         self.z0, self.nzl = plan.planes(s)
         self.slab = SlabStencil(op, self.z0, self.z0 + self.nzl)
         self.device = device
-        self.stream = E.stream_ptr(device)
+        with torch.cuda.device(device):
+            self.torch_stream = torch.cuda.current_stream(device)
+        self.stream = ctypes.c_void_p(self.torch_stream.cuda_stream)
         self.dm = device_matrix(self.slab, device, self.stream)
         self.ldv = E.block_ldv(n_vec)
         nx, ny, _ = op.shape
@@ -131,6 +134,14 @@ class DeviceSlab:
                      self.own(prev) if prev is not None else None, self.own(nxt), self.own(v0),
                      E.ptr(self.partials), self.partials.numel() * 8, self.stream)
 
+    def step_halo(self, k, c, d, cur, prev, nxt, v0, halo_lo, halo_hi):
+        """Step whose kernel epilogue also stores the first / last own plane of
+        w_{k+1} into the neighbours' ghost planes (tensors on this or a peer
+        device) -- the fused compute + halo exchange."""
+        _native.call("sdb_cheb_step_halo", self.dm.handle, c, d, self.n_vec, self.degree, self.mode, k,
+                     self.own(cur), self.own(prev) if prev is not None else None, self.own(nxt), self.own(v0),
+                     E.ptr(self.partials), self.partials.numel() * 8, E.ptr(halo_lo), E.ptr(halo_hi), self.stream)
+
     def reduce(self):
         import torch
 
@@ -138,6 +149,55 @@ class DeviceSlab:
         _native.call("sdb_cheb_reduce", self.dm.handle, self.n_vec, self.degree, self.mode, E.ptr(self.partials),
                      E.ptr(zeta_pp), self.stream)
         return zeta_pp
+
+
+def run_rowpartition_p2p(slabs, plan, c, d, degree, mode):
+    """All slabs in this process (one or several devices): every step kernel
+    pushes its boundary planes straight into the neighbours' ghost planes (no
+    separate exchange, no NCCL).  Step k+1 of a slab waits for its two
+    neighbours' step k (stream order on one device, CUDA events across
+    devices): their pushes have landed in its ghosts and they are done reading
+    the ghosts it is about to overwrite."""
+    import torch
+
+    steps = (degree + 1) // 2 if mode == _native.SDB_CHEB_DOUBLING else degree
+    by_id = {sl.s: sl for sl in slabs}
+    if set(by_id) != set(range(plan.n_slabs)):
+        raise ValueError("the p2p exchange needs every slab in this process")
+    devices = sorted({sl.device for sl in slabs})
+    for a in devices:
+        for b in devices:
+            _native.call("sdb_enable_peer_access", a, b)
+    multi = len(devices) > 1
+    cur = {s: by_id[s].blocks[0] for s in by_id}
+    prev = {s: None for s in by_id}
+    done = {}
+    for k in range(max(steps, 1)):
+        nxt = {s: by_id[s].blocks[1] if k == 0 else (by_id[s].blocks[2] if k == 1 else prev[s]) for s in by_id}
+        push = steps > 0 and k + 1 < steps
+        events = {}
+        for s, sl in by_id.items():
+            lo, hi = plan.neighbours(s)
+            if multi and k > 0:
+                for nb in {lo, hi}:
+                    sl.torch_stream.wait_event(done[nb])
+            if push:
+                sl.step_halo(k, c, d, cur[s], prev[s], nxt[s], sl.blocks[0], nxt[lo][-1], nxt[hi][0])
+            else:
+                sl.step(k, c, d, cur[s], prev[s], nxt[s], sl.blocks[0])
+            if multi:
+                ev = torch.cuda.Event()
+                ev.record(sl.torch_stream)
+                events[s] = ev
+        done = events
+        prev, cur = cur, nxt
+    total = None
+    for s in sorted(by_id):
+        if multi:
+            torch.cuda.current_stream(slabs[0].device).wait_stream(by_id[s].torch_stream)
+        z = by_id[s].reduce().to(slabs[0].device)
+        total = z if total is None else total + z
+    return total
 
 
 def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=None):
@@ -171,11 +231,14 @@ def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=N
 
 
 def rowpartition_moments(op, interval, degree, source, n_vec, mode=_native.SDB_CHEB_DOUBLING, n_slabs=None,
-                         group=None, device=None):
+                         group=None, device=None, devices=None, exchange="p2p"):
     """Per-probe moments of (A - cI)/d for a periodic StencilOperator with the
-    z-planes row-partitioned: one slab per rank of ``group`` (or ``n_slabs``
-    slabs in this process when no group is given -- the single-GPU form used
-    by the tests).  Returns a (n_vec, degree+1) device tensor."""
+    z-planes row-partitioned: one slab per rank of ``group`` (NCCL send/recv of
+    the halo planes), or ``n_slabs`` slabs in this process spread over
+    ``devices`` (default: the one device) with the halo pushed by the step
+    kernels themselves over peer memory (``exchange="p2p"``; ``"copy"``: the
+    step kernels plus device-to-device plane copies).  Returns a
+    (n_vec, degree+1) tensor on the first device."""
     import torch
     import torch.distributed as dist
 
@@ -197,10 +260,17 @@ def rowpartition_moments(op, interval, degree, source, n_vec, mode=_native.SDB_C
         rank_of_slab = None
     if min(plan.planes(s)[1] for s in range(plan.n_slabs)) < 1:
         raise ValueError("more slabs than z-planes")
-    with torch.cuda.device(device):
-        slabs = [DeviceSlab(op, plan, s, n_vec, degree, mode, device) for s in local]
-        for sl in slabs:
+    devs = [device] if (devices is None or rank_of_slab is not None) else [int(x) for x in devices]
+    slabs = []
+    for s in local:
+        dev = devs[s % len(devs)]
+        with torch.cuda.device(dev):
+            sl = DeviceSlab(op, plan, s, n_vec, degree, mode, dev)
             ghosted_probe_block(source, 0, n_vec, op.shape, sl.z0, sl.nzl, sl.ldv, sl.blocks[0])
+        slabs.append(sl)
+    with torch.cuda.device(device):
+        if rank_of_slab is None and exchange == "p2p":
+            return run_rowpartition_p2p(slabs, plan, c, d, degree, mode)
         return run_rowpartition(slabs, plan, c, d, degree, mode, group if rank_of_slab else None, rank_of_slab)
 
 

@@ -1,6 +1,8 @@
 """Row-partitioned stencil moments on the GPU: z-ghost slab kernels, several
-slabs driven in one process (halo planes exchanged by device copies).  The
-multi-rank exchange itself is covered on CPU (tests/test_rowpart_cpu.py)."""
+slabs driven in one process, halo planes pushed by the step kernels into the
+neighbours' ghost planes (p2p: the same code path that writes peer-device
+memory over NVLink when the slabs sit on several GPUs) or exchanged by device
+copies.  The multi-rank NCCL exchange is covered on CPU (tests/test_rowpart_cpu.py)."""
 
 import numpy as np
 import pytest
@@ -23,12 +25,13 @@ def generic_stencil():
                          ids=["face7", "box27", "generic"])
 @pytest.mark.parametrize("n_slabs", [1, 2, 3, 4])
 @pytest.mark.parametrize("mode", [1, 0], ids=["doubling", "direct"])
-def test_slabs_match_oracle(builder, n_slabs, mode):
+@pytest.mark.parametrize("exchange", ["p2p", "copy"])
+def test_slabs_match_oracle(builder, n_slabs, mode, exchange):
     op = builder()
     iv = W.gershgorin_interval(op)
     n_vec, deg = 20, 31
     src = sdb.ProbeVectorSource("rademacher", seed=4, dim=op.dim)
-    got = rowpartition_moments(op, iv, deg, src, n_vec, mode=mode, n_slabs=n_slabs).cpu().numpy()
+    got = rowpartition_moments(op, iv, deg, src, n_vec, mode=mode, n_slabs=n_slabs, exchange=exchange).cpu().numpy()
     ref = O.chebyshev_moments(op.csr, iv.center, iv.halfwidth, deg, "rademacher", 4, n_vec, mode="direct")
     assert np.max(np.abs(got - ref)) <= 1e-10 * np.max(np.abs(ref))
 
@@ -39,5 +42,18 @@ def test_slabs_match_unpartitioned_large():
     src = sdb.ProbeVectorSource("rademacher", seed=0, dim=op.dim)
     whole = sdb.moments_via_product_formula(sdb.apply_spectral_map(op, iv), 60, src, 32)
     for n_slabs in (2, 8):
-        got = rowpartition_moments(op, iv, 60, src, 32, n_slabs=n_slabs).mean(dim=0).cpu().numpy()
-        assert np.max(np.abs(got - whole.zeta)) <= 1e-12 * np.max(np.abs(whole.zeta))
+        for exchange in ("p2p", "copy"):
+            got = rowpartition_moments(op, iv, 60, src, 32, n_slabs=n_slabs, exchange=exchange)
+            got = got.mean(dim=0).cpu().numpy()
+            assert np.max(np.abs(got - whole.zeta)) <= 1e-12 * np.max(np.abs(whole.zeta))
+
+
+def test_p2p_devices_list_single_gpu():
+    """The multi-device p2p driver (events between slab streams) with every
+    slab on device 0: same moments as the single-device path."""
+    op = W.anderson_3d(8)
+    iv = W.gershgorin_interval(op)
+    src = sdb.ProbeVectorSource("rademacher", seed=1, dim=op.dim)
+    a = rowpartition_moments(op, iv, 21, src, 16, n_slabs=3, devices=[0, 0]).cpu().numpy()
+    b = rowpartition_moments(op, iv, 21, src, 16, n_slabs=3, exchange="copy").cpu().numpy()
+    np.testing.assert_array_equal(a, b)
