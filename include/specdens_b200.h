@@ -283,6 +283,18 @@ SDB_API int sdb_blur_nodes(const double* theta, const double* w, int64_t count, 
                    int kind, double width, const double* grid, int64_t n_pts, double* density,
                    void* stream);
 
+/* ---- Matrix Market ingestion (matrix.py:247-304) --------- */
+/* Host-side reader (no CUDA calls): parses a real/integer coordinate file with a
+ * symmetric or general header into an expanded CSR (both triangles, columns
+ * sorted per row, duplicates summed in file order), checks exact symmetry;
+ * errors are SDB_EINVAL with the reference's ValueError messages.  The CSR is
+ * copied out with sdb_mm_export and uploaded like any other matrix. */
+typedef struct sdb_mm sdb_mm;
+SDB_API int sdb_mm_read(const char* path, sdb_mm** out);
+SDB_API int sdb_mm_info(const sdb_mm* mm, int64_t* n, int64_t* nnz, int32_t* symmetric_storage);
+SDB_API int sdb_mm_export(const sdb_mm* mm, int64_t* indptr, int32_t* indices, double* values);
+SDB_API void sdb_mm_free(sdb_mm* mm);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,6 +84,10 @@ SIGNATURES = {
     "sdb_haydock": (_i, [_p, _p, _p, _p, _i64, _i64, _p, _i64, _d, _p, _p, _p, _p]),
     "sdb_tridiag_resolvent": (_i, [_p, _p, _i64, _p, _i64, _p, _p, _p, _p, _p]),
     "sdb_dgl": (_i, [_p, _i64, _p, _i64, _d, _d, _d, _p, _p, _p, _p, _p, _p]),
+    "sdb_mm_read": (_i, [ctypes.c_char_p, ctypes.POINTER(_p)]),
+    "sdb_mm_info": (_i, [_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_int32)]),
+    "sdb_mm_export": (_i, [_p, _p, _p, _p]),
+    "sdb_mm_free": (None, [_p]),
     "sdb_cheb_kernel": (ctypes.c_char_p, [_p, _i64, _i]),
     "sdb_cheb_moments": (_i, [_p, _d, _d, _i64, _i64, _i, _p, _p, _p, _sz, _p, ctypes.POINTER(ctypes.c_float)]),
     "sdb_cheb_partials_size": (_i, [_p, _i64, _i64, _i, ctypes.POINTER(_sz)]),

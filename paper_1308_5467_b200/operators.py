@@ -564,3 +564,43 @@ def estimate_spectral_interval(op, lanczos_steps=DEFAULT_LANCZOS_STEPS, margin=D
         half = max(abs(ub), 1.0) * 1e-8
         lb, ub = lb - half, ub + half
     return SpectralInterval(lb, ub).widened(margin)
+
+
+# ---------------------------------------------------------------------------
+# Matrix Market coordinate IO (matrix.py:247-331): the reader
+# is native (libspecdens_b200 ``sdb_mm_read``: parse, expand, sum duplicates,
+# exact symmetry check); the matrix then uploads to the device like any CSR.
+
+
+def load_matrix_market(path):
+    """Read a real coordinate Matrix Market file into a SparseSymmetricMatrix
+    (same accepted headers, expansion, duplicate summing and ValueErrors as
+    matrix.py:247-304)."""
+    lib = _native.load()
+    h = ctypes.c_void_p()
+    _native.check(lib.sdb_mm_read(os.fsencode(str(path)), ctypes.byref(h)))
+    try:
+        n, nnz, sym = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int32()
+        _native.check(lib.sdb_mm_info(h, ctypes.byref(n), ctypes.byref(nnz), ctypes.byref(sym)))
+        indptr = np.empty(n.value + 1, dtype=np.int64)
+        indices = np.empty(nnz.value, dtype=np.int32)
+        data = np.empty(nnz.value, dtype=np.float64)
+        _native.check(lib.sdb_mm_export(h, indptr.ctypes.data, indices.ctypes.data, data.ctypes.data))
+    finally:
+        lib.sdb_mm_free(h)
+    if nnz.value < 2**31 - 1:  # SciPy wants one index dtype for indptr and indices
+        indptr = indptr.astype(np.int32)
+    else:
+        indices = indices.astype(np.int64)
+    csr = sp.csr_array((data, indices, indptr), shape=(n.value, n.value))
+    return SparseSymmetricMatrix(csr=csr, symmetric_storage=bool(sym.value))
+
+
+def save_matrix_market(mat, path):
+    """Write the lower triangle as a real symmetric coordinate file (matrix.py:321-331)."""
+    coo = sp.tril(mat.csr).tocoo()
+    with open(path, "w", encoding="ascii") as fh:
+        fh.write("%%MatrixMarket matrix coordinate real symmetric\n")
+        fh.write(f"{mat.n} {mat.n} {coo.nnz}\n")
+        for i, j, v in zip(coo.row, coo.col, coo.data):
+            fh.write(f"{i + 1} {j + 1} {float(v)!r}\n")

@@ -228,6 +228,42 @@ def haydock_case(name, op, kind, n_vec, steps, n_pts, eta):
                 w_first=w0, w_last=wl, matrix_sha256=csr_digest(mat.csr), n=mat.dim)
 
 
+MM_FILES = {
+    "tridiag_sym.mtx": "%%MatrixMarket matrix coordinate real symmetric\n3 3 5\n1 1 2.0\n2 1 -1.0\n2 2 2.0\n"
+                       "3 2 -1.0\n3 3 2.0\n",
+    "dup_sym.mtx": "%%MatrixMarket matrix coordinate real symmetric\n2 2 3\n1 1 1.5\n1 1 0.5\n2 1 -1.0\n",
+    "general_comments.mtx": "%%MatrixMarket matrix coordinate real general\n% a comment\n\n4 4 7\n"
+                            "1 1 1e-3\n% inner comment\n1 2 -2.5\n2 1 -2.5\n2 2 4\n3 4 0.125\n"
+                            "4 3 0.125\n\n4 4 -7.0E+2\n",
+    "integer_upper.mtx": "%%MatrixMarket MATRIX Coordinate INTEGER Symmetric\n3 3 4\n1 1 3\n3 1 -1\n2 2 +5\n"
+                         "3 3 2\n",
+    "zero.mtx": "%%MatrixMarket matrix coordinate real symmetric\n4 4 0\n",
+}
+
+
+def mm_case(name):
+    """load_matrix_market / save_matrix_market (matrix.py:247-331) on small files."""
+    from specdens.matrix import generate_modified_laplacian_2d, load_matrix_market, save_matrix_market
+
+    d = os.path.join(HERE, "mm")
+    os.makedirs(d, exist_ok=True)
+    for fname, text in MM_FILES.items():
+        with open(os.path.join(d, fname), "w", encoding="ascii") as fh:
+            fh.write(text)
+    save_matrix_market(generate_modified_laplacian_2d(20, 15), os.path.join(d, "lap20x15.mtx"))
+    out = {}
+    for fname in sorted(os.listdir(d)):
+        mat = load_matrix_market(os.path.join(d, fname))
+        key = fname.replace(".mtx", "")
+        out[f"{key}_indptr"] = mat.csr.indptr.astype(np.int64)
+        out[f"{key}_indices"] = mat.csr.indices.astype(np.int64)
+        out[f"{key}_data"] = mat.csr.data
+        out[f"{key}_symmetric_storage"] = mat.symmetric_storage
+    out["files"] = np.array(sorted(os.listdir(d)))
+    print(f"{name}: {len(out['files'])} files", flush=True)
+    return out
+
+
 def main():
     meta = dict(numpy=np.__version__, scipy=scipy.__version__, specdens=specdens.__version__,
                 python=sys.version.split()[0])
@@ -241,6 +277,7 @@ def main():
         "haydock_small": lambda: haydock_case("haydock_small", W.anderson_3d(8), "gaussian", 6, 40, 400, 0.05),
         "haydock_c4": lambda: haydock_case("haydock_c4", W.build_matrix("C4"), "gaussian", 4, 100, 2000, 0.01),
         "interval": lambda: interval_case("interval"),
+        "matrix_market": lambda: mm_case("matrix_market"),
         "variants_c1": lambda: variants_case("variants_c1", W.build_matrix("C1"), "gaussian", 20, 100, 1000),
         "variants_c5small": lambda: variants_case("variants_c5small", W.stencil27_3d(24), "rademacher", 32, 60,
                                                   500),
