@@ -16,6 +16,8 @@
 //   K5a lz_proj    h = V_{0..j}^T w (one warp per basis vector t streaming its
 //                  rows; the first projection also applies w -= alpha v_j)
 //   K5b lz_update  w -= V_{0..j} h, optional ||w||^2 partials
+//   K5c lz_update_proj  full reorth: pass 1's update and pass 2's projection
+//                  in one basis read (3 basis passes per step instead of 4)
 // and small fixed-order reduce kernels between them (deterministic).  A probe
 // that breaks down is frozen (1/beta = 0) while the others continue.
 #include <cmath>
@@ -284,6 +286,102 @@ __global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
   }
 }
 
+// ---- K5c: fused CGS2 middle pass: w -= V h1, then h2 partials = V^T w -------
+// The classical schedule reads the basis four times per step (proj, update,
+// proj, update).  The update of pass 1 and the projection of pass 2 touch the
+// same basis entries V[t][i][:] for a row i, and the new w[i] depends only on
+// row i, so one pass can do both: load V[t][i][cols] for every t <= j into
+// registers, form s = sum_t V h1, w' = w - s (block reduce over t-groups),
+// then accumulate h2[t] += V[t][i] w'[i] from the same registers.  The basis
+// is read once instead of twice; the step reads it 3x in total.
+// Block (row block rb, column slice cs): kZcs column pairs x kZtg t-groups;
+// thread (c, tg) owns t = tg + kZtg*k, k < KMAX (KMAX*kZtg >= j+1) and keeps
+// those h1 values and h2 accumulators in registers.  kZrows rows per
+// iteration keep 2*KMAX independent 16-byte loads in flight per thread.
+constexpr int kZcs = 16;
+
+template <int KMAX, int kZrows, int kZtg>
+__global__ void __launch_bounds__(kZcs * kZtg, (KMAX * kZrows * kZtg >= 256) ? 1 : 2)
+    lz_update_proj(const double* __restrict__ basis, double* __restrict__ w, const double* __restrict__ h, int64_t j,
+                   int64_t n, int64_t ldv, int64_t nrb, double* __restrict__ partials) {
+  const int c = threadIdx.x % kZcs, tg = threadIdx.x / kZcs;
+  const int64_t rb = blockIdx.y;  // column slices of the same rows run side by side
+  const int64_t col = 2 * ((int64_t)blockIdx.x * kZcs + c);
+  const bool colok = col < ldv;
+  const int64_t rs = n * rb / nrb, re = n * (rb + 1) / nrb;
+  const size_t plane = (size_t)n * ldv;
+  extern __shared__ double2 h1s[];  // [KMAX * kZtg][kZcs]: this block's column slice of h1
+  __shared__ double2 red[kZrows][kZtg][kZcs];
+  __shared__ double2 wn[kZrows][kZcs];
+  for (int idx = threadIdx.x; idx < KMAX * kZtg * kZcs; idx += blockDim.x) {
+    const int64_t t = idx / kZcs, cc = 2 * ((int64_t)blockIdx.x * kZcs + idx % kZcs);
+    h1s[idx] = (t <= j && cc < ldv) ? ld_d2(h + t * ldv + cc) : make_double2(0.0, 0.0);
+  }
+  double2 acc[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) acc[k] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int64_t r0 = rs; r0 < re; r0 += kZrows) {
+    double2 v[kZrows][KMAX];
+    double2 wv = make_double2(0.0, 0.0);
+    const bool wown = tg < kZrows && colok && r0 + tg < re;
+    if (wown) wv = ld_d2(w + (r0 + tg) * ldv + col);  // in flight with the basis loads
+#pragma unroll
+    for (int r = 0; r < kZrows; ++r)
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        const int64_t t = tg + (int64_t)kZtg * k;
+        v[r][k] = (colok && t <= j && r0 + r < re) ? ld_d2_stream(basis + (size_t)t * plane + (r0 + r) * ldv + col)
+                                                    : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+    for (int r = 0; r < kZrows; ++r) {
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        const double2 hh = h1s[(tg + kZtg * k) * kZcs + c];
+        s.x = fma(v[r][k].x, hh.x, s.x);
+        s.y = fma(v[r][k].y, hh.y, s.y);
+      }
+      red[r][tg][c] = s;
+    }
+    __syncthreads();
+    if (tg < kZrows) {
+      const int r = tg;
+      double2 s = red[r][0][c];
+#pragma unroll
+      for (int g = 1; g < kZtg; ++g) {
+        s.x += red[r][g][c].x;
+        s.y += red[r][g][c].y;
+      }
+      wv.x -= s.x;
+      wv.y -= s.y;
+      if (wown) st_d2(w + (r0 + r) * ldv + col, wv);
+      wn[r][c] = wv;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kZrows; ++r) {
+      const double2 x = wn[r][c];
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k) {
+        acc[k].x = fma(v[r][k].x, x.x, acc[k].x);
+        acc[k].y = fma(v[r][k].y, x.y, acc[k].y);
+      }
+    }
+  }
+  if (!colok) return;
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    const int64_t t = tg + (int64_t)kZtg * k;
+    if (t <= j) {
+      double* p = partials + ((size_t)t * nrb + rb) * ldv + col;
+      p[0] = acc[k].x;
+      p[1] = acc[k].y;
+    }
+  }
+}
+
 // reorth = "none": w' = w - alpha v_j into wdst, ||w'||^2 partials.
 template <int L, int VPL>
 __global__ void __launch_bounds__(kRowThreads) lz_sub_alpha_norm(const double* __restrict__ vj,
@@ -420,6 +518,40 @@ static int lz_launch_update(const Geometry& g, bool norm, const double* basis, d
   return SDB_OK;
 }
 
+// Fused middle pass when the per-thread t range fits the register budget.
+template <int KM, int RW, int TG>
+static void lz_upj_launch(dim3 grid, const double* basis, double* w, const double* h, int64_t j, int64_t n,
+                          int64_t ldv, int64_t nrb, double* part, cudaStream_t s) {
+  const size_t smem = (size_t)KM * TG * kZcs * sizeof(double2);
+  static bool attr = false;
+  if (!attr && smem > 48 * 1024) {
+    cudaFuncSetAttribute(lz_update_proj<KM, RW, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  lz_update_proj<KM, RW, TG><<<grid, kZcs * TG, smem, s>>>(basis, w, h, j, n, ldv, nrb, part);
+}
+
+static bool lz_launch_update_proj(const double* basis, double* w, const double* h, int64_t j, int64_t n, int64_t ldv,
+                                  int64_t nrb, double* part, cudaStream_t s) {
+  dim3 grid((unsigned)((ldv / 2 + kZcs - 1) / kZcs), (unsigned)nrb);
+  const int64_t T = j + 1;
+#define SDB_UPJ(KM, RW, TG)                                                  \
+  if (T <= (int64_t)KM * TG) {                                               \
+    lz_upj_launch<KM, RW, TG>(grid, basis, w, h, j, n, ldv, nrb, part, s);  \
+    return true;                                                             \
+  }
+  // two rows per iteration (measured best on C4: 16 t-groups x 2 rows beats
+  // 1 row, 4 rows and 32 t-groups)
+  SDB_UPJ(1, 2, 16) SDB_UPJ(2, 2, 16) SDB_UPJ(4, 2, 16) SDB_UPJ(8, 2, 16) SDB_UPJ(16, 1, 16)
+#undef SDB_UPJ
+  return false;
+}
+
+static bool lz_fused_enabled() {
+  const char* e = getenv("SDB_LZ_FUSED");
+  return !(e && e[0] == '0');
+}
+
 }  // namespace sdb
 
 using namespace sdb;
@@ -480,6 +612,7 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
   CsrView cv{};
   if (m->format == SDB_FMT_CSR) cv = make_csr_view(m); else sv = make_stencil_view(m);
 
+  const bool fused = lz_fused_enabled();
   const double* wraw = v0;
   for (int64_t j = 0; j < steps; ++j) {
     double* vj = basis + (size_t)j * plane;
@@ -505,10 +638,13 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
       SDB_CHECK_LAUNCH();
       lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
       SDB_CHECK_LAUNCH();
-      if ((rc = lz_launch_update(g, false, basis, W0, h, j, n, nrb, panel, part, s))) return rc;
-      SDB_CHECK_LAUNCH();
-      // pass 2: h = V^T w; w -= V h; ||w||^2
-      if ((rc = lz_launch_proj(nv, false, false, basis, W0, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
+      // pass 2: h = V^T w; w -= V h; ||w||^2  (update of pass 1 + projection
+      // of pass 2 fused into one basis read when the t range fits registers)
+      if (!(fused && lz_launch_update_proj(basis, W0, h, j, n, ldv, nrb, part, s))) {
+        if ((rc = lz_launch_update(g, false, basis, W0, h, j, n, nrb, panel, part, s))) return rc;
+        SDB_CHECK_LAUNCH();
+        if ((rc = lz_launch_proj(nv, false, false, basis, W0, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
+      }
       SDB_CHECK_LAUNCH();
       lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
       SDB_CHECK_LAUNCH();

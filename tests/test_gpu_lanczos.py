@@ -193,3 +193,28 @@ def test_lanczos_nonfinite_raises():
     op = sdb.SparseSymmetricMatrix.from_dense(np.array([[np.inf, 0.0], [0.0, 1.0]]))
     with pytest.raises(sdb.NumericalFailure, match="non-finite Lanczos"):
         sdb.lanczos_factorize(op, np.ones(2), 2)
+
+
+@pytest.mark.parametrize("steps", [5, 40, 100, 300])
+def test_fused_cgs2_pass_matches_four_pass_schedule(monkeypatch, steps):
+    """The fused update+projection pass (K5c) against the unfused 4-pass CGS2
+    schedule on the same probes: same math, only the summation order differs.
+    300 steps exceeds the fused kernel's register range and takes the fallback."""
+    op = W.anderson_3d(12)
+    iv = W.gershgorin_interval(op)
+    src = sdb.ProbeVectorSource("gaussian", seed=3, dim=op.dim)
+    grid = sdb.interval_grid(iv, 256)
+    monkeypatch.setenv("SDB_LZ_FUSED", "1")
+    fused = sdb.lanczos_dos(op, iv, steps, src, 70, 0.05, grid)
+    monkeypatch.setenv("SDB_LZ_FUSED", "0")
+    plain = sdb.lanczos_dos(op, iv, steps, src, 70, 0.05, grid)
+    assert np.max(np.abs(fused.density - plain.density)) <= 1e-10
+    np.testing.assert_allclose(fused.params["ritz_nodes"], plain.params["ritz_nodes"], rtol=0, atol=1e-10)
+    if steps <= 100:
+        monkeypatch.setenv("SDB_LZ_FUSED", "1")
+        for l in (0, 69):
+            alpha, beta = O.lanczos_factorize(op.csr, src.draw(l), steps)[:2]
+            f = sdb.lanczos_factorize(op, src.draw(l), steps)
+            scale = np.max(np.abs(alpha))
+            assert np.max(np.abs(f.alpha - alpha)) <= 1e-10 * scale
+            assert np.max(np.abs(f.beta - beta)) <= 1e-10 * scale

@@ -1,0 +1,4 @@
+# Lanczos fused middle pass + C3 probe-batch sweep
+timeout 600 python -m pytest tests/test_gpu_lanczos.py tests/test_gpu_haydock.py tests/test_gpu_interval.py -x -q > gpurun_out/pytest_lz.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_lz.log
+for f in 1 0; do SDB_LZ_FUSED=$f timeout 300 python tools/config_bench.py C4 --reps 2 2>&1 | tail -1 | sed "s/^/fused=$f /"; done
+for b in 128 64 32 16 8; do SDB_BATCH=$b timeout 300 python tools/config_bench.py C3 --reps 1 2>&1 | tail -1 | sed "s/^/batch=$b /"; done
