@@ -13,6 +13,13 @@ one above its own planes.  Per recurrence step:
      this process, an NCCL send/recv pair otherwise (2 x nx*ny*ldv*8 bytes
      received per slab per step: 33.6 MB at 256^3 with 32 probes).
 
+With an exchange between ranks (NCCL) the step is split so the transfer
+overlaps the bulk of the SpMM: the slab's first and last own planes are
+computed first (two single-plane z-ghost handles on the same block memory),
+the halo send/recv of those planes is issued on a communication stream, and
+the interior planes are computed on the compute stream meanwhile.  The next
+step's boundary planes wait for the exchange; its interior does not need it.
+
 Moments are sums over rows, so each slab reduces its own partials into
 per-probe moments and one all-reduce over ranks at the end gives the global
 per-probe moments (the doubling transform is linear, so it commutes with the
@@ -124,6 +131,20 @@ class DeviceSlab:
                                                             __import__("ctypes").byref(need)))
         self.partials = torch.empty(max(need.value, 8) // 8 + 1, dtype=torch.float64, device=device)
         self.n_vec, self.degree, self.mode = n_vec, degree, mode
+        # boundary / interior split (overlapped exchange): single-plane handles
+        # for the first and last own plane, one for the planes between them;
+        # each part owns a partials buffer, its moments are summed in reduce()
+        self.parts = {}
+        if self.nzl >= 3:
+            spans = {"lo": (0, 1), "int": (1, self.nzl - 1), "hi": (self.nzl - 1, self.nzl)}
+            for name, (a, b) in spans.items():
+                sub = SlabStencil(op, self.z0 + a, self.z0 + b)
+                dm = device_matrix(sub, device, self.stream)
+                _native.check(_native.load().sdb_cheb_partials_size(dm.handle, n_vec, degree, mode,
+                                                                    ctypes.byref(need)))
+                part = torch.empty(max(need.value, 8) // 8 + 1, dtype=torch.float64, device=device)
+                self.parts[name] = (sub, dm, a, part)
+        self.split_used = False
 
     def own(self, t):
         """Pointer to the first own row of a ghosted block."""
@@ -142,9 +163,28 @@ class DeviceSlab:
                      self.own(cur), self.own(prev) if prev is not None else None, self.own(nxt), self.own(v0),
                      E.ptr(self.partials), self.partials.numel() * 8, E.ptr(halo_lo), E.ptr(halo_hi), self.stream)
 
+    def step_part(self, name, k, c, d, cur, prev, nxt, v0):
+        """Step of one part ('lo', 'int', 'hi') of the slab's own planes: the
+        part's handle reads its z neighbours from the adjacent planes of the
+        same ghosted block (own planes, or the slab's ghost planes at the ends)."""
+        _, dm, a, part = self.parts[name]
+        row = lambda t: E.ptr(t[1 + a])  # noqa: E731
+        _native.call("sdb_cheb_step", dm.handle, c, d, self.n_vec, self.degree, self.mode, k, row(cur),
+                     row(prev) if prev is not None else None, row(nxt), row(v0), E.ptr(part), part.numel() * 8,
+                     self.stream)
+        self.split_used = True
+
     def reduce(self):
         import torch
 
+        if self.split_used:
+            total = None
+            for _, dm, _, part in self.parts.values():
+                z = torch.empty((self.n_vec, self.degree + 1), dtype=torch.float64, device=self.device)
+                _native.call("sdb_cheb_reduce", dm.handle, self.n_vec, self.degree, self.mode, E.ptr(part),
+                             E.ptr(z), self.stream)
+                total = z if total is None else total + z
+            return total
         zeta_pp = torch.empty((self.n_vec, self.degree + 1), dtype=torch.float64, device=self.device)
         _native.call("sdb_cheb_reduce", self.dm.handle, self.n_vec, self.degree, self.mode, E.ptr(self.partials),
                      E.ptr(zeta_pp), self.stream)
@@ -200,27 +240,60 @@ def run_rowpartition_p2p(slabs, plan, c, d, degree, mode):
     return total
 
 
-def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=None):
+def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=None, overlap=True):
     """Drive the recurrence over local slab objects (DeviceSlab or a CPU
     stand-in with the same interface: .blocks (3 ghosted blocks, block 0 holds
-    the probes), .step(k, c, d, cur, prev, next, v0), .reduce()).
+    the probes), .step(k, c, d, cur, prev, next, v0), .reduce(); optionally
+    .parts / .step_part(name, ...) for the boundary / interior split).
+
+    With ``overlap`` and slabs that can split (>= 3 planes each), every step
+    runs the boundary planes, starts the halo exchange on a communication
+    stream (CUDA slabs) and runs the interior planes while it is in flight.
 
     Returns the per-probe moments of the whole grid (sum over all slabs,
     all-reduced over ``group`` when slabs live on several ranks)."""
+    import torch
     import torch.distributed as dist
 
     steps = (degree + 1) // 2 if mode == _native.SDB_CHEB_DOUBLING else degree
     ids = [sl.s for sl in slabs]
+    split = overlap and steps > 1 and all(getattr(sl, "parts", None) for sl in slabs)
+    devs = {getattr(sl, "device", None) for sl in slabs}
+    dev = next(iter(devs))
+    if split and len(devs) > 1:
+        split = False  # one compute stream per process: the split needs the slabs on one device
+    cuda = split and isinstance(dev, int)
+    if cuda:
+        compute = slabs[0].torch_stream
+        comm = torch.cuda.Stream(device=dev)
     cur = {sl.s: sl.blocks[0] for sl in slabs}
     prev = {sl.s: None for sl in slabs}
     for k in range(max(steps, 1)):
-        nxt = {}
-        for sl in slabs:
-            nxt[sl.s] = sl.blocks[1] if k == 0 else (sl.blocks[2] if k == 1 else prev[sl.s])
-            sl.step(k, c, d, cur[sl.s], prev[sl.s], nxt[sl.s], sl.blocks[0])
-        if steps > 0 and k + 1 < steps:
-            halo_exchange(ids, plan, nxt, group, rank_of_slab)
+        nxt = {sl.s: sl.blocks[1] if k == 0 else (sl.blocks[2] if k == 1 else prev[sl.s]) for sl in slabs}
+        exchange = steps > 0 and k + 1 < steps
+        if not split:
+            for sl in slabs:
+                sl.step(k, c, d, cur[sl.s], prev[sl.s], nxt[sl.s], sl.blocks[0])
+            if exchange:
+                halo_exchange(ids, plan, nxt, group, rank_of_slab)
+        else:
+            if cuda and k > 0:
+                compute.wait_stream(comm)  # ghosts of w_k have landed
+            for sl in slabs:
+                for part in ("lo", "hi"):
+                    sl.step_part(part, k, c, d, cur[sl.s], prev[sl.s], nxt[sl.s], sl.blocks[0])
+            if exchange:
+                if cuda:
+                    comm.wait_stream(compute)  # boundary planes of w_{k+1} are written
+                    with torch.cuda.stream(comm):
+                        halo_exchange(ids, plan, nxt, group, rank_of_slab)
+                else:
+                    halo_exchange(ids, plan, nxt, group, rank_of_slab)
+            for sl in slabs:  # interior planes overlap the exchange
+                sl.step_part("int", k, c, d, cur[sl.s], prev[sl.s], nxt[sl.s], sl.blocks[0])
         prev, cur = cur, nxt
+    if cuda:
+        compute.wait_stream(comm)
     total = None
     for sl in slabs:
         z = sl.reduce()
@@ -231,13 +304,14 @@ def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=N
 
 
 def rowpartition_moments(op, interval, degree, source, n_vec, mode=_native.SDB_CHEB_DOUBLING, n_slabs=None,
-                         group=None, device=None, devices=None, exchange="p2p"):
+                         group=None, device=None, devices=None, exchange="p2p", overlap=True):
     """Per-probe moments of (A - cI)/d for a periodic StencilOperator with the
     z-planes row-partitioned: one slab per rank of ``group`` (NCCL send/recv of
     the halo planes), or ``n_slabs`` slabs in this process spread over
     ``devices`` (default: the one device) with the halo pushed by the step
     kernels themselves over peer memory (``exchange="p2p"``; ``"copy"``: the
-    step kernels plus device-to-device plane copies).  Returns a
+    step kernels plus device-to-device plane copies, overlapped with the
+    interior planes when ``overlap``).  Returns a
     (n_vec, degree+1) tensor on the first device."""
     import torch
     import torch.distributed as dist
@@ -271,7 +345,8 @@ def rowpartition_moments(op, interval, degree, source, n_vec, mode=_native.SDB_C
     with torch.cuda.device(device):
         if rank_of_slab is None and exchange == "p2p":
             return run_rowpartition_p2p(slabs, plan, c, d, degree, mode)
-        return run_rowpartition(slabs, plan, c, d, degree, mode, group if rank_of_slab else None, rank_of_slab)
+        return run_rowpartition(slabs, plan, c, d, degree, mode, group if rank_of_slab else None, rank_of_slab,
+                                overlap=overlap)
 
 
 def prepare_rowpartition(op, interval, degree, source, n_vec, mode=_native.SDB_CHEB_DOUBLING, group=None,

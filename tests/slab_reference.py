@@ -19,11 +19,16 @@ class NumpySlab:
         shape = (self.nzl + 2, self.nxy, n_vec)
         self.blocks = [torch.zeros(shape, dtype=torch.float64) for _ in range(3)]
         self.raw = np.zeros((degree + 1, n_vec))
+        # boundary / interior split, as rowpart.DeviceSlab.parts
+        self.parts = {"lo": (0, 1), "int": (1, self.nzl - 1), "hi": (self.nzl - 1, self.nzl)} if self.nzl >= 3 else {}
+
+    def step_part(self, name, k, c, d, cur, prev, nxt, v0):
+        self.step(k, c, d, cur, prev, nxt, v0, planes=self.parts[name])
 
     def _own(self, t):
         return t[1:-1].numpy().reshape(self.nzl, self.ny, self.nx, self.n_vec)
 
-    def step(self, k, c, d, cur, prev, nxt, v0):
+    def step(self, k, c, d, cur, prev, nxt, v0, planes=None):
         g = cur.numpy().reshape(self.nzl + 2, self.ny, self.nx, self.n_vec)
         x = g[1:-1]
         y = self.diag[..., None] * x
@@ -36,7 +41,9 @@ class NumpySlab:
             wn = t
         else:
             wn = 2.0 * t - self._own(prev)
-        nxt[1:-1] = torch.from_numpy(wn.reshape(self.nzl, self.nxy, self.n_vec))
+        a, b = planes if planes is not None else (0, self.nzl)
+        wn, x = wn[a:b], x[a:b]
+        nxt[1 + a:1 + b] = torch.from_numpy(wn.reshape(b - a, self.nxy, self.n_vec))
         red = lambda a, b: np.einsum("zyxl,zyxl->l", a, b)  # noqa: E731
         if self.doubling:
             if k == 0:
@@ -46,7 +53,7 @@ class NumpySlab:
             if 2 * k + 2 <= self.degree:
                 self.raw[2 * k + 2] += red(wn, wn)
         else:
-            p = self._own(v0)
+            p = self._own(v0)[a:b]
             if k == 0:
                 self.raw[0] += red(p, p)
             self.raw[k + 1] += red(p, wn)

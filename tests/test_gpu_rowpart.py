@@ -57,3 +57,18 @@ def test_p2p_devices_list_single_gpu():
     a = rowpartition_moments(op, iv, 21, src, 16, n_slabs=3, devices=[0, 0]).cpu().numpy()
     b = rowpartition_moments(op, iv, 21, src, 16, n_slabs=3, exchange="copy").cpu().numpy()
     np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("mode", [1, 0], ids=["doubling", "direct"])
+def test_boundary_interior_split_matches_whole_slab_steps(mode):
+    """Copy exchange with the boundary / interior split (exchange on a second
+    stream overlapping the interior planes) against whole-slab steps."""
+    op = W.stencil27_3d(16)
+    iv = W.gershgorin_interval(op)
+    src = sdb.ProbeVectorSource("rademacher", seed=2, dim=op.dim)
+    for n_slabs in (1, 2, 4):
+        a = rowpartition_moments(op, iv, 41, src, 24, mode=mode, n_slabs=n_slabs, exchange="copy",
+                                 overlap=True).cpu().numpy()
+        b = rowpartition_moments(op, iv, 41, src, 24, mode=mode, n_slabs=n_slabs, exchange="copy",
+                                 overlap=False).cpu().numpy()
+        assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(b))

@@ -33,7 +33,8 @@ def probes(op, n_vec):
 
 @pytest.mark.parametrize("n_slabs", [1, 2, 3, 5])
 @pytest.mark.parametrize("doubling", [True, False])
-def test_single_process_slabs(n_slabs, doubling):
+@pytest.mark.parametrize("overlap", [True, False])
+def test_single_process_slabs(n_slabs, doubling, overlap):
     from tests.slab_reference import NumpySlab, fill_probes
 
     op = W.stencil27_3d(6) if n_slabs % 2 else W.anderson_3d(7)
@@ -44,7 +45,8 @@ def test_single_process_slabs(n_slabs, doubling):
     slabs = [NumpySlab(op, plan, s, n_vec, DEG, doubling) for s in range(n_slabs)]
     for sl in slabs:
         fill_probes(sl, pr, op.shape)
-    got = run_rowpartition(slabs, plan, iv.center, iv.halfwidth, DEG, 1 if doubling else 0).numpy()
+    got = run_rowpartition(slabs, plan, iv.center, iv.halfwidth, DEG, 1 if doubling else 0, overlap=overlap).numpy()
+    assert all(sl.parts for sl in slabs) == (op.shape[2] // n_slabs >= 3)
     assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))
 
 
@@ -54,7 +56,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, overlap):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -67,14 +69,16 @@ def _worker(rank, world, port, q):
         plan = SlabPlan(op.shape[2], world)
         sl = NumpySlab(op, plan, rank, n_vec, DEG, True)
         fill_probes(sl, probes(op, n_vec), op.shape)
+        assert sl.parts  # 3 planes per slab: the boundary / interior split applies
         got = run_rowpartition([sl], plan, iv.center, iv.halfwidth, DEG, 1, group=None,
-                               rank_of_slab=lambda s: s)
+                               rank_of_slab=lambda s: s, overlap=overlap)
         q.put((rank, got.numpy()))
     finally:
         dist.destroy_process_group()
 
 
-def test_two_rank_halo_exchange_gloo():
+@pytest.mark.parametrize("overlap", [True, False])
+def test_two_rank_halo_exchange_gloo(overlap):
     import sys
 
     ctx = mp.get_context("spawn")
@@ -83,7 +87,7 @@ def test_two_rank_halo_exchange_gloo():
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     if root not in sys.path:
         sys.path.insert(0, root)
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, overlap)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=180) for _ in procs)
