@@ -187,6 +187,28 @@ SDB_API int sdb_cheb_step_halo(const sdb_matrix* m, double c, double d, int64_t 
 SDB_API int sdb_enable_peer_access(int device, int peer);
 SDB_API int sdb_cheb_reduce(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode, const double* partials,
                     double* zeta_pp, void* stream);
+/* Plane-range steps on the z-march layout (row partition of a periodic 7/27-
+ * point grid): every rank holds full-size ghost-padded blocks
+ * [nz][ny+2][nx+2][ldv] of the whole grid but computes only its own planes
+ * [z_lo, z_hi) of w_{k+1}, reading x = w_k on planes z_lo-1 .. z_hi (periodic;
+ * the two neighbour planes are the halo the caller exchanged) -- the TMA
+ * z-march kernel of sdb_cheb_moments restricted to a plane range.
+ * sdb_zm_block_info: doubles per padded plane and bytes per block (0 and 0
+ * when the z-march layout does not apply: then use sdb_cheb_step on z-slab
+ * handles).  sdb_zm_pad_probes: n x ldv probe block -> padded block.
+ * sdb_cheb_step_planes: step k on the planes [z_lo, z_hi) (x/prev/next/v0 are
+ * padded blocks; next may alias prev); sdb_cheb_reduce_planes: the partials
+ * of all steps of that same range -> per-probe moments (linear in the planes,
+ * so ranges and ranks add up).  partial_bytes as sdb_cheb_partials_size. */
+SDB_API int sdb_zm_block_info(const sdb_matrix* m, int64_t n_vec, int mode, int64_t* plane_doubles,
+                              size_t* block_bytes);
+SDB_API int sdb_zm_pad_probes(const sdb_matrix* m, int64_t n_vec, const double* probes, double* padded, void* stream);
+SDB_API int sdb_cheb_step_planes(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode,
+                                 int64_t k, int64_t z_lo, int64_t z_hi, const double* x, const double* prev,
+                                 double* next, const double* v0, double* partials, size_t partial_bytes,
+                                 void* stream);
+SDB_API int sdb_cheb_reduce_planes(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode, int64_t z_lo,
+                                   int64_t z_hi, const double* partials, double* zeta_pp, void* stream);
 /* zeta[k] = (1/n_vec) sum_l zeta_pp[l][k], probes summed in index order
  * (kpm.py:135, :193).  nonfinite (device int32, may be NULL) is set to 1 if
  * any zeta[k] is not finite. */

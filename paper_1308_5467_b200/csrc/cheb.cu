@@ -978,6 +978,95 @@ int sdb_cheb_reduce(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode
   return launch_reduce(P, n_vec, degree, mode, partials, zeta_pp, (cudaStream_t)stream);
 }
 
+int sdb_zm_block_info(const sdb_matrix* m, int64_t n_vec, int mode, int64_t* plane_doubles, size_t* block_bytes) {
+  SDB_REQUIRE(m && plane_doubles && block_bytes, "NULL argument");
+  SDB_REQUIRE(n_vec >= 1 && n_vec <= SDB_MAX_BATCH, "n_vec must lie in [1, %d] per batch", SDB_MAX_BATCH);
+  int leg_;
+  mode = split_mode(mode, &leg_);
+  const int64_t ldv = choose_geometry(n_vec).ldv;
+  ZmPlan zp;
+  int rc = zm_plan(m, ldv, mode, &zp);
+  if (rc) return rc;
+  *plane_doubles = 0;
+  *block_bytes = 0;
+  if (!zp.on || zp.fuse) return SDB_OK;
+  *plane_doubles = (m->st.ny + 2 * zp.G) * (m->st.nx + 2 * zp.G) * ldv;
+  *block_bytes = zp.block_bytes;
+  return SDB_OK;
+}
+
+int sdb_zm_pad_probes(const sdb_matrix* m, int64_t n_vec, const double* probes, double* padded, void* stream) {
+  SDB_REQUIRE(m && probes && padded, "NULL argument");
+  SDB_REQUIRE(n_vec >= 1 && n_vec <= SDB_MAX_BATCH, "n_vec must lie in [1, %d] per batch", SDB_MAX_BATCH);
+  const int64_t ldv = choose_geometry(n_vec).ldv;
+  ZmPlan zp;
+  int rc = zm_plan(m, ldv, SDB_CHEB_DOUBLING, &zp);
+  if (rc) return rc;
+  SDB_REQUIRE(zp.on && !zp.fuse, "the z-march layout does not apply to this matrix");
+  DeviceGuard dg(m->device);
+  if (!dg.ok) return fail(SDB_ECUDA, "cannot select CUDA device %d", m->device);
+  return zm_pad(m, zp, probes, ldv, padded, (cudaStream_t)stream);
+}
+
+int sdb_cheb_step_planes(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode, int64_t k,
+                         int64_t z_lo, int64_t z_hi, const double* x, const double* prev, double* next,
+                         const double* v0, double* partials, size_t partial_bytes, void* stream) {
+  SDB_REQUIRE(m && x && next && partials, "NULL argument");
+  int legendre;
+  mode = split_mode(mode, &legendre);
+  size_t pb = 0;
+  int rc = sdb_cheb_partials_size(m, n_vec, degree, mode, &pb);
+  if (rc) return rc;
+  SDB_REQUIRE(partial_bytes >= pb, "partials buffer too small (%zu < %zu bytes)", partial_bytes, pb);
+  const int64_t steps = (mode == SDB_CHEB_DOUBLING) ? (degree + 1) / 2 : degree;
+  SDB_REQUIRE(k >= 0 && k < steps, "step %lld outside [0, %lld)", (long long)k, (long long)steps);
+  SDB_REQUIRE(k == 0 || prev != nullptr, "prev must not be NULL after the first step");
+  SDB_REQUIRE(mode != SDB_CHEB_DIRECT || v0 != nullptr || k == 0, "direct mode needs v0");
+  SDB_REQUIRE(d != 0.0, "spectral halfwidth must be non-zero");
+  DeviceGuard dg(m->device);
+  if (!dg.ok) return fail(SDB_ECUDA, "cannot select CUDA device %d", m->device);
+  StepPlan P;
+  if ((rc = plan_steps(m, n_vec, mode, c, d, &P))) return rc;
+  ZmPlan zp;
+  if ((rc = zm_plan_range(m, P.g.ldv, mode, z_lo, z_hi, &zp))) return rc;
+  SDB_REQUIRE(zp.on, "no z-march plan for planes [%lld, %lld) of this matrix", (long long)z_lo, (long long)z_hi);
+  StepArgs a = P.a;
+  a.legendre = legendre;
+  a.partials = partials;
+  a.v0 = v0 ? v0 : x;
+  a.x = x;
+  a.prev = prev;
+  a.next = next;
+  a.slot0 = (k == 0) ? 0 : -1;
+  set_step_scalars(a, k);
+  if (mode == SDB_CHEB_DOUBLING) {
+    a.slotB = (2 * k + 1 <= degree) ? (int)(2 * k + 1) : -1;
+    a.slotA = (2 * k + 2 <= degree) ? (int)(2 * k + 2) : -1;
+  } else {
+    a.slotA = (int)(k + 1);
+    a.slotB = -1;
+  }
+  return zm_launch_step(m, zp, a, k == 0, mode, (cudaStream_t)stream);
+}
+
+int sdb_cheb_reduce_planes(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode, int64_t z_lo, int64_t z_hi,
+                           const double* partials, double* zeta_pp, void* stream) {
+  int leg_;
+  mode = split_mode(mode, &leg_);
+  SDB_REQUIRE(m && partials && zeta_pp, "NULL argument");
+  SDB_REQUIRE(n_vec >= 1 && n_vec <= SDB_MAX_BATCH && degree >= 0, "bad shape");
+  DeviceGuard dg(m->device);
+  if (!dg.ok) return fail(SDB_ECUDA, "cannot select CUDA device %d", m->device);
+  StepPlan P;
+  int rc = plan_steps(m, n_vec, mode, 0.0, 1.0, &P);
+  if (rc) return rc;
+  ZmPlan zp;
+  if ((rc = zm_plan_range(m, P.g.ldv, mode, z_lo, z_hi, &zp))) return rc;
+  SDB_REQUIRE(zp.on, "no z-march plan for planes [%lld, %lld) of this matrix", (long long)z_lo, (long long)z_hi);
+  P.a.nblocks = zp.nbp;
+  return launch_reduce(P, n_vec, degree, mode, partials, zeta_pp, (cudaStream_t)stream);
+}
+
 int sdb_moments_mean(const double* zeta_pp, int64_t n_vec, int64_t degree, double* zeta, int32_t* nonfinite,
                      void* stream) {
   SDB_REQUIRE(zeta_pp && zeta, "NULL argument");

@@ -97,9 +97,14 @@ struct ZmPlan {
   size_t smem2 = 0;        // their dynamic shared memory
   int R2 = 0;              // and ring depth
   int G = 1;               // ghost width of the padded blocks (2 with fused pairs)
+  int z_lo = 0, z_hi = 0;  // planes computed per launch
   const char* name = "";
 };
 int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* p);
+// Plan for the planes [z_lo, z_hi) only (row partition on full-size padded
+// blocks: the other planes are neither read, except the two neighbour
+// planes, nor written).  Off (p->on false) when the range is empty.
+int zm_plan_range(const sdb_matrix* m, int64_t ldv, int mode, int64_t z_lo, int64_t z_hi, ZmPlan* p);
 // w_{k+1} = step(x = w_k, prev = w_{k-1}) on padded blocks; partial rows p.nbp.
 int zm_launch_step(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, bool first, int mode, cudaStream_t s);
 // Fused pair of doubling-mode steps k, k+1: x = w_k, prev = w_{k-1} (unused

@@ -49,6 +49,7 @@ struct ZmArgs {
   int R;                      // ring slots
   int64_t items;              // n_xt * n_yt * n_zs * slices
   int G;                      // ghost width of the padded blocks (1, or 2 with fused pairs)
+  int z_lo, z_hi;             // planes computed: [z_lo, z_hi) (row partition: a slab's planes)
   const double* diag;         // n (unpadded)
   double wc[27];              // weights, lexicographic (dz, dy, dx); centre unused
 };
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
         sp /= t.n_xt;
         const int yt = (int)(sp % t.n_yt);
         const int zs = (int)(sp / t.n_yt);
-        const int zbeg = zs * t.ZS, zend = min(zbeg + t.ZS, nz);
+        const int zbeg = t.z_lo + zs * t.ZS, zend = min(zbeg + t.ZS, t.z_hi);
         const int c0 = slice * CS, x0 = xt * TX, y0 = yt * TY;
         for (int p = zbeg - 1; p <= zend; ++p) {
           if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
     sp /= t.n_xt;
     const int yt = (int)(sp % t.n_yt);
     const int zs = (int)(sp / t.n_yt);
-    const int zbeg = zs * t.ZS, zend = min(zbeg + t.ZS, nz);
+    const int zbeg = t.z_lo + zs * t.ZS, zend = min(zbeg + t.ZS, t.z_hi);
     col0 = slice * CS;
     pb_row = (int)(blockIdx.x / t.slices);
     // this thread's columns: point index g + k*GROUPS of the TX x TY tile
@@ -441,7 +442,7 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
         sp /= t.n_xt;
         const int yt = (int)(sp % t.n_yt);
         const int zs = (int)(sp / t.n_yt);
-        const int zbeg = zs * t.ZS, zend = min(zbeg + t.ZS, nz);
+        const int zbeg = t.z_lo + zs * t.ZS, zend = min(zbeg + t.ZS, t.z_hi);
         const int c0 = slice * CS, x0 = xt * TX, y0 = yt * TY;
         for (int p = zbeg - 2; p <= zend + 1; ++p) {
           if (use > 0) mbar_wait(empty + s, (use - 1) & 1);
@@ -479,7 +480,7 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
     sp /= t.n_xt;
     const int yt = (int)(sp % t.n_yt);
     const int zs = (int)(sp / t.n_yt);
-    const int zbeg = zs * t.ZS, zend = min(zbeg + t.ZS, nz);
+    const int zbeg = t.z_lo + zs * t.ZS, zend = min(zbeg + t.ZS, t.z_hi);
     col0 = slice * CS;
     pb_row = (int)(blockIdx.x / t.slices);
     const int x0 = xt * TX, y0 = yt * TY;
@@ -812,6 +813,10 @@ static bool zm_fits(const ZmCfg& c, int nx, int ny, int64_t ldv) {
 }
 
 int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* out) {
+  return zm_plan_range(m, ldv, mode, 0, m->format == SDB_FMT_STENCIL ? m->st.nz : 0, out);
+}
+
+int zm_plan_range(const sdb_matrix* m, int64_t ldv, int mode, int64_t z_lo, int64_t z_hi, ZmPlan* out) {
   int leg_;
   mode = split_mode(mode, &leg_);
   ZmPlan p;
@@ -822,6 +827,10 @@ int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* out) {
   if (!zm_env("SDB_ZMARCH", 1)) return SDB_OK;
   const int nx = (int)m->st.nx, ny = (int)m->st.ny, nz = (int)m->st.nz;
   if (nx < 2 * kZmGhost || ny < 2 * kZmGhost || nz < 3) return SDB_OK;  // ghost images must not overlap
+  if (z_lo < 0 || z_hi > nz || z_lo >= z_hi) return SDB_OK;
+  const int nzr = (int)(z_hi - z_lo);  // planes this plan computes
+  p.z_lo = (int)z_lo;
+  p.z_hi = (int)z_hi;
   int cfg = -1;
   const int forced = zm_env("SDB_ZM_CFG", -1);
   if (forced >= 0 && forced < kZmNumCfgs) {
@@ -859,10 +868,11 @@ int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* out) {
   int nzs = zm_env("SDB_ZM_NZS", 0);
   if (nzs <= 0) {
     nzs = (int)((4LL * sms + base - 1) / base);
-    if (nzs > nz / 4) nzs = nz / 4 > 0 ? nz / 4 : 1;
+    if (nzs > nzr / 4) nzs = nzr / 4 > 0 ? nzr / 4 : 1;
   }
-  p.ZS = (nz + nzs - 1) / nzs;
-  p.n_zs = (nz + p.ZS - 1) / p.ZS;
+  if (nzs > nzr) nzs = nzr;
+  p.ZS = (nzr + nzs - 1) / nzs;
+  p.n_zs = (nzr + p.ZS - 1) / p.ZS;
   p.items = base * p.n_zs;
   // persistent grid: a multiple of the slice count, at most one block per SM,
   // the largest one that minimises the busiest block's item count
@@ -886,7 +896,7 @@ int zm_plan(const sdb_matrix* m, int64_t ldv, int mode, ZmPlan* out) {
   // r01_zmarch_sweep.txt) -- the per-plane stage barrier serialises the 8
   // consumer warps and the halo recompute adds 56 % stage-1 work, while the
   // single-step kernel already streams at ~85 % of HBM peak
-  if (mode == SDB_CHEB_DOUBLING && zm_env("SDB_ZM_FUSE", 0) && (cfg == 0 || cfg == 2 || cfg == 3 || cfg == 5)) {
+  if (nzr == nz && mode == SDB_CHEB_DOUBLING && zm_env("SDB_ZM_FUSE", 0) && (cfg == 0 || cfg == 2 || cfg == 3 || cfg == 5)) {
     const int64_t slot2 = zm_slot2_doubles(c, false);
     const int64_t ring = zm_w1ring_doubles(c);
     int R2 = (int)((int64_t)(budget - 256 - ring * sizeof(double)) / (slot2 * (int64_t)sizeof(double)));
@@ -965,6 +975,8 @@ int zm_launch_step(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, bool
   t.R = p.R;
   t.items = p.items;
   t.G = p.G;
+  t.z_lo = p.z_lo;
+  t.z_hi = p.z_hi;
   t.diag = m->diag;
   for (int o = 0; o < 27; ++o) t.wc[o] = o < m->nterms ? m->term_w_host[o] : 0.0;
   StepArgs aa = a;
@@ -1024,6 +1036,8 @@ int zm_launch_pair(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, cons
   t.slices = (int)(a.ldv / c.CS);
   t.R = p.R2;
   t.items = p.items;
+  t.z_lo = 0;
+  t.z_hi = nz;
   t.diag = m->diag;
   for (int o = 0; o < 27; ++o) t.wc[o] = o < m->nterms ? m->term_w_host[o] : 0.0;
   StepArgs aa = a;

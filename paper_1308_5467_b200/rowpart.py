@@ -191,6 +191,127 @@ class DeviceSlab:
         return zeta_pp
 
 
+class PlaneSlab:
+    """One slab on one GPU in the z-march layout (periodic 7/27-point grids):
+    full-size ghost-padded blocks [nz][ny+2][nx+2][ldv] of the whole grid, of
+    which this slab computes its own planes [z0, z0+nzl) with the TMA z-march
+    kernel restricted to that range (``sdb_cheb_step_planes``) and holds valid
+    data only there plus the two neighbour planes the exchange fills.  The
+    unused planes cost memory only (3 x 4.4 GB at 256^3 x 32 probes, of 180 GB).
+
+    Parts: first own plane, interior, last own plane (``step_part``), so the
+    boundary planes can be exchanged while the interior is computed."""
+
+    def __init__(self, op, plan, s, n_vec, degree, mode, device, info=None):
+        import torch
+
+        self.s = s
+        self.z0, self.nzl = plan.planes(s)
+        self.nz = op.shape[2]
+        self.device = device
+        with torch.cuda.device(device):
+            self.torch_stream = torch.cuda.current_stream(device)
+        self.stream = ctypes.c_void_p(self.torch_stream.cuda_stream)
+        self.dm = device_matrix(op, device, self.stream)
+        pd, bb = info if info is not None else plane_layout(self.dm, n_vec, mode)
+        if pd == 0:
+            raise TypeError("the z-march layout does not apply to this operator")
+        self.plane_doubles = pd
+        self.n_vec, self.degree, self.mode = n_vec, degree, mode
+        self.ldv = E.block_ldv(n_vec)
+        flat = [torch.empty(bb // 8, dtype=torch.float64, device=device) for _ in range(3)]
+        for f in flat[1:]:
+            f.fill_(float("nan"))  # planes the exchange does not fill must never be read
+        self.blocks = [f[:self.nz * pd].view(self.nz, pd) for f in flat]
+        z0, z1 = self.z0, self.z0 + self.nzl
+        if self.nzl >= 3:
+            self.parts = {"lo": (z0, z0 + 1), "int": (z0 + 1, z1 - 1), "hi": (z1 - 1, z1)}
+        else:
+            self.parts = {}
+        need = ctypes.c_size_t()
+        _native.check(_native.load().sdb_cheb_partials_size(self.dm.handle, n_vec, degree, mode, ctypes.byref(need)))
+        self.partials = {name: torch.empty(max(need.value, 8) // 8 + 1, dtype=torch.float64, device=device)
+                         for name in list(self.parts) + ["all"]}  # one partials buffer per plane range
+        self.used = set()
+
+    def stage_probes(self, source):
+        """Probes 0..n_vec-1 (drawn on the host as the reference does) -> padded block 0."""
+        staged = E.stage_probes(source, 0, self.n_vec, int(source.dim), self.device, self.stream)
+        _native.call("sdb_zm_pad_probes", self.dm.handle, self.n_vec, E.ptr(staged.block), E.ptr(self.blocks[0]),
+                     self.stream)
+        self._keep = staged
+
+    def _step(self, name, z_lo, z_hi, k, c, d, cur, prev, nxt, v0):
+        part = self.partials[name]
+        _native.call("sdb_cheb_step_planes", self.dm.handle, c, d, self.n_vec, self.degree, self.mode, k, z_lo, z_hi,
+                     E.ptr(cur), E.ptr(prev) if prev is not None else None, E.ptr(nxt), E.ptr(v0), E.ptr(part),
+                     part.numel() * 8, self.stream)
+        self.used.add((name, z_lo, z_hi))
+
+    def step(self, k, c, d, cur, prev, nxt, v0):
+        self._step("all", self.z0, self.z0 + self.nzl, k, c, d, cur, prev, nxt, v0)
+
+    def step_part(self, name, k, c, d, cur, prev, nxt, v0):
+        z_lo, z_hi = self.parts[name]
+        self._step(name, z_lo, z_hi, k, c, d, cur, prev, nxt, v0)
+
+    def reduce(self):
+        import torch
+
+        total = None
+        for name, z_lo, z_hi in sorted(self.used):
+            z = torch.empty((self.n_vec, self.degree + 1), dtype=torch.float64, device=self.device)
+            _native.call("sdb_cheb_reduce_planes", self.dm.handle, self.n_vec, self.degree, self.mode, z_lo, z_hi,
+                         E.ptr(self.partials[name]), E.ptr(z), self.stream)
+            total = z if total is None else total + z
+        return total
+
+
+def plane_layout(dm, n_vec, mode):
+    """(doubles per padded plane, bytes per padded block); (0, 0) when the
+    z-march layout does not apply (non-grid stencil, CSR, odd shapes)."""
+    pd, bb = ctypes.c_int64(), ctypes.c_size_t()
+    _native.check(_native.load().sdb_zm_block_info(dm.handle, n_vec, mode, ctypes.byref(pd), ctypes.byref(bb)))
+    return pd.value, bb.value
+
+
+def plane_exchange(slabs, plan, blocks, group=None, rank_of_slab=None):
+    """Halo exchange on full-size blocks: slab s receives plane z0-1 from its
+    lower neighbour and plane z0+nzl from its upper neighbour (periodic), each
+    stored at the same global plane index; local slabs copy, remote slabs use
+    NCCL send/recv (sends first, lower then upper; receives upper then lower,
+    so any world size, including 2, matches)."""
+    import torch.distributed as dist
+
+    by_s = {sl.s: sl for sl in slabs}
+    nz = plan.nz
+    for sl in slabs:
+        lo, hi = plan.neighbours(sl.s)
+        below, above = (sl.z0 - 1) % nz, (sl.z0 + sl.nzl) % nz
+        if lo in by_s and lo != sl.s:
+            blocks[sl.s][below].copy_(blocks[lo][below])
+        if hi in by_s and hi != sl.s:
+            blocks[sl.s][above].copy_(blocks[hi][above])
+    if rank_of_slab is None:
+        return
+    ops = []
+    for sl in slabs:
+        lo, hi = plan.neighbours(sl.s)
+        if lo not in by_s:
+            ops.append(dist.P2POp(dist.isend, blocks[sl.s][sl.z0], rank_of_slab(lo), group))
+        if hi not in by_s:
+            ops.append(dist.P2POp(dist.isend, blocks[sl.s][sl.z0 + sl.nzl - 1], rank_of_slab(hi), group))
+    for sl in slabs:
+        lo, hi = plan.neighbours(sl.s)
+        if hi not in by_s:
+            ops.append(dist.P2POp(dist.irecv, blocks[sl.s][(sl.z0 + sl.nzl) % nz], rank_of_slab(hi), group))
+        if lo not in by_s:
+            ops.append(dist.P2POp(dist.irecv, blocks[sl.s][(sl.z0 - 1) % nz], rank_of_slab(lo), group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
+
 def run_rowpartition_p2p(slabs, plan, c, d, degree, mode):
     """All slabs in this process (one or several devices): every step kernel
     pushes its boundary planes straight into the neighbours' ghost planes (no
@@ -240,15 +361,16 @@ def run_rowpartition_p2p(slabs, plan, c, d, degree, mode):
     return total
 
 
-def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=None, overlap=True):
+def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=None, overlap=None):
     """Drive the recurrence over local slab objects (DeviceSlab or a CPU
     stand-in with the same interface: .blocks (3 ghosted blocks, block 0 holds
     the probes), .step(k, c, d, cur, prev, next, v0), .reduce(); optionally
     .parts / .step_part(name, ...) for the boundary / interior split).
 
-    With ``overlap`` and slabs that can split (>= 3 planes each), every step
-    runs the boundary planes, starts the halo exchange on a communication
-    stream (CUDA slabs) and runs the interior planes while it is in flight.
+    With ``overlap`` (default: when slabs live on several ranks) and slabs
+    that can split (>= 3 planes each), every step runs the boundary planes,
+    starts the halo exchange on a communication stream (CUDA slabs) and runs
+    the interior planes while it is in flight.
 
     Returns the per-probe moments of the whole grid (sum over all slabs,
     all-reduced over ``group`` when slabs live on several ranks)."""
@@ -256,7 +378,17 @@ def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=N
     import torch.distributed as dist
 
     steps = (degree + 1) // 2 if mode == _native.SDB_CHEB_DOUBLING else degree
+    if overlap is None:
+        overlap = rank_of_slab is not None
     ids = [sl.s for sl in slabs]
+    full = hasattr(slabs[0], "plane_doubles")  # full-size z-march blocks (PlaneSlab)
+
+    def exchange_halo(nxt):
+        if full:
+            plane_exchange(slabs, plan, nxt, group, rank_of_slab)
+        else:
+            halo_exchange(ids, plan, nxt, group, rank_of_slab)
+
     split = overlap and steps > 1 and all(getattr(sl, "parts", None) for sl in slabs)
     devs = {getattr(sl, "device", None) for sl in slabs}
     dev = next(iter(devs))
@@ -266,6 +398,11 @@ def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=N
     if cuda:
         compute = slabs[0].torch_stream
         comm = torch.cuda.Stream(device=dev)
+    for sl in slabs:  # which partial buffers this run fills (reduce() sums exactly those)
+        if hasattr(sl, "used"):
+            sl.used.clear()
+        if hasattr(sl, "split_used"):
+            sl.split_used = False
     cur = {sl.s: sl.blocks[0] for sl in slabs}
     prev = {sl.s: None for sl in slabs}
     for k in range(max(steps, 1)):
@@ -275,7 +412,7 @@ def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=N
             for sl in slabs:
                 sl.step(k, c, d, cur[sl.s], prev[sl.s], nxt[sl.s], sl.blocks[0])
             if exchange:
-                halo_exchange(ids, plan, nxt, group, rank_of_slab)
+                exchange_halo(nxt)
         else:
             if cuda and k > 0:
                 compute.wait_stream(comm)  # ghosts of w_k have landed
@@ -286,9 +423,9 @@ def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=N
                 if cuda:
                     comm.wait_stream(compute)  # boundary planes of w_{k+1} are written
                     with torch.cuda.stream(comm):
-                        halo_exchange(ids, plan, nxt, group, rank_of_slab)
+                        exchange_halo(nxt)
                 else:
-                    halo_exchange(ids, plan, nxt, group, rank_of_slab)
+                    exchange_halo(nxt)
             for sl in slabs:  # interior planes overlap the exchange
                 sl.step_part("int", k, c, d, cur[sl.s], prev[sl.s], nxt[sl.s], sl.blocks[0])
         prev, cur = cur, nxt
@@ -303,15 +440,37 @@ def run_rowpartition(slabs, plan, c, d, degree, mode, group=None, rank_of_slab=N
     return total
 
 
+def make_slab(op, plan, s, n_vec, degree, mode, device, source, planes=True):
+    """Slab s with its probes staged: a PlaneSlab (z-march on full-size padded
+    blocks) when ``planes`` and the layout applies, else a DeviceSlab."""
+    import torch
+
+    with torch.cuda.device(device):
+        if planes:
+            stream = ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+            info = plane_layout(device_matrix(op, device, stream), n_vec, mode)
+            if info[0] > 0:
+                sl = PlaneSlab(op, plan, s, n_vec, degree, mode, device, info)
+                sl.stage_probes(source)
+                return sl
+        sl = DeviceSlab(op, plan, s, n_vec, degree, mode, device)
+        ghosted_probe_block(source, 0, n_vec, op.shape, sl.z0, sl.nzl, sl.ldv, sl.blocks[0])
+        return sl
+
+
 def rowpartition_moments(op, interval, degree, source, n_vec, mode=_native.SDB_CHEB_DOUBLING, n_slabs=None,
-                         group=None, device=None, devices=None, exchange="p2p", overlap=True):
+                         group=None, device=None, devices=None, exchange="p2p", overlap=None, layout="auto"):
     """Per-probe moments of (A - cI)/d for a periodic StencilOperator with the
     z-planes row-partitioned: one slab per rank of ``group`` (NCCL send/recv of
     the halo planes), or ``n_slabs`` slabs in this process spread over
     ``devices`` (default: the one device) with the halo pushed by the step
     kernels themselves over peer memory (``exchange="p2p"``; ``"copy"``: the
-    step kernels plus device-to-device plane copies, overlapped with the
-    interior planes when ``overlap``).  Returns a
+    step kernels plus device-to-device plane copies).  ``overlap``: split each
+    step so the exchange runs beside the interior planes (default: only across
+    ranks -- on one device the plane copies are cheaper than the split, which
+    measured +8 % per step at 256^3).  ``layout``: "planes" (full-size z-march
+    blocks, PlaneSlab), "slabs" (ghosted slab blocks, DeviceSlab) or "auto"
+    (planes for the copy / NCCL exchange when the z-march applies).  Returns a
     (n_vec, degree+1) tensor on the first device."""
     import torch
     import torch.distributed as dist
@@ -335,16 +494,13 @@ def rowpartition_moments(op, interval, degree, source, n_vec, mode=_native.SDB_C
     if min(plan.planes(s)[1] for s in range(plan.n_slabs)) < 1:
         raise ValueError("more slabs than z-planes")
     devs = [device] if (devices is None or rank_of_slab is not None) else [int(x) for x in devices]
-    slabs = []
-    for s in local:
-        dev = devs[s % len(devs)]
-        with torch.cuda.device(dev):
-            sl = DeviceSlab(op, plan, s, n_vec, degree, mode, dev)
-            ghosted_probe_block(source, 0, n_vec, op.shape, sl.z0, sl.nzl, sl.ldv, sl.blocks[0])
-        slabs.append(sl)
+    use_planes = layout == "planes" or (layout == "auto" and (exchange != "p2p" or rank_of_slab is not None))
+    slabs = [make_slab(op, plan, s, n_vec, degree, mode, devs[s % len(devs)], source, use_planes) for s in local]
     with torch.cuda.device(device):
-        if rank_of_slab is None and exchange == "p2p":
+        if rank_of_slab is None and exchange == "p2p" and not hasattr(slabs[0], "plane_doubles"):
             return run_rowpartition_p2p(slabs, plan, c, d, degree, mode)
+        if overlap is None:
+            overlap = rank_of_slab is not None
         return run_rowpartition(slabs, plan, c, d, degree, mode, group if rank_of_slab else None, rank_of_slab,
                                 overlap=overlap)
 
@@ -361,9 +517,7 @@ def prepare_rowpartition(op, interval, degree, source, n_vec, mode=_native.SDB_C
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     plan = SlabPlan(nz, world)
-    with torch.cuda.device(device):
-        sl = DeviceSlab(op, plan, rank, n_vec, degree, mode, device)
-        ghosted_probe_block(source, 0, n_vec, op.shape, sl.z0, sl.nzl, sl.ldv, sl.blocks[0])
+    sl = make_slab(op, plan, rank, n_vec, degree, mode, device, source, True)
     return [sl], plan, ((lambda s: s) if world > 1 else None)
 
 

@@ -55,7 +55,7 @@ def test_p2p_devices_list_single_gpu():
     iv = W.gershgorin_interval(op)
     src = sdb.ProbeVectorSource("rademacher", seed=1, dim=op.dim)
     a = rowpartition_moments(op, iv, 21, src, 16, n_slabs=3, devices=[0, 0]).cpu().numpy()
-    b = rowpartition_moments(op, iv, 21, src, 16, n_slabs=3, exchange="copy").cpu().numpy()
+    b = rowpartition_moments(op, iv, 21, src, 16, n_slabs=3, exchange="copy", layout="slabs").cpu().numpy()
     np.testing.assert_array_equal(a, b)
 
 
@@ -68,7 +68,40 @@ def test_boundary_interior_split_matches_whole_slab_steps(mode):
     src = sdb.ProbeVectorSource("rademacher", seed=2, dim=op.dim)
     for n_slabs in (1, 2, 4):
         a = rowpartition_moments(op, iv, 41, src, 24, mode=mode, n_slabs=n_slabs, exchange="copy",
-                                 overlap=True).cpu().numpy()
+                                 overlap=True, layout="slabs").cpu().numpy()
         b = rowpartition_moments(op, iv, 41, src, 24, mode=mode, n_slabs=n_slabs, exchange="copy",
-                                 overlap=False).cpu().numpy()
+                                 overlap=False, layout="slabs").cpu().numpy()
         assert np.max(np.abs(a - b)) <= 1e-12 * np.max(np.abs(b))
+
+
+@pytest.mark.parametrize("builder", [lambda: W.anderson_3d(16), lambda: W.stencil27_3d(16)], ids=["face7", "box27"])
+@pytest.mark.parametrize("n_slabs", [1, 2, 3, 4])
+@pytest.mark.parametrize("mode", [1, 0], ids=["doubling", "direct"])
+@pytest.mark.parametrize("overlap", [True, False])
+def test_plane_range_zmarch_slabs(builder, n_slabs, mode, overlap):
+    """Row partition on full-size z-march blocks (sdb_cheb_step_planes): each
+    slab computes its planes with the TMA z-march kernel; planes it does not
+    own start as NaN, so a missing halo plane would poison the moments."""
+    from paper_1308_5467_b200 import rowpart as RP
+
+    op = builder()
+    iv = W.gershgorin_interval(op)
+    src = sdb.ProbeVectorSource("rademacher", seed=6, dim=op.dim)
+    plan = RP.SlabPlan(op.shape[2], n_slabs)
+    assert isinstance(RP.make_slab(op, plan, 0, 32, 31, mode, 0, src, True), RP.PlaneSlab)
+    got = rowpartition_moments(op, iv, 31, src, 32, mode=mode, n_slabs=n_slabs, exchange="copy", overlap=overlap,
+                               layout="planes").cpu().numpy()
+    ref = O.chebyshev_moments(op.csr, iv.center, iv.halfwidth, 31, "rademacher", 6, 32, mode="direct")
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got - ref)) <= 1e-10 * np.max(np.abs(ref))
+
+
+def test_plane_range_matches_unpartitioned_large():
+    op = W.stencil27_3d(32)
+    iv = W.gershgorin_interval(op)
+    src = sdb.ProbeVectorSource("rademacher", seed=0, dim=op.dim)
+    whole = sdb.moments_via_product_formula(sdb.apply_spectral_map(op, iv), 60, src, 32)
+    for n_slabs in (2, 8):
+        got = rowpartition_moments(op, iv, 60, src, 32, n_slabs=n_slabs, exchange="copy", layout="planes")
+        got = got.mean(dim=0).cpu().numpy()
+        assert np.max(np.abs(got - whole.zeta)) <= 1e-12 * np.max(np.abs(whole.zeta))

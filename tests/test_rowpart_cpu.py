@@ -56,19 +56,23 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q, overlap):
+def _worker(rank, world, port, q, overlap, planes=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from tests.slab_reference import NumpySlab, fill_probes
+        from tests.slab_reference import NumpyPlaneSlab, NumpySlab, fill_plane_probes, fill_probes
 
         op = W.anderson_3d(6)
         n_vec = 2
         iv = W.gershgorin_interval(op)
         plan = SlabPlan(op.shape[2], world)
-        sl = NumpySlab(op, plan, rank, n_vec, DEG, True)
-        fill_probes(sl, probes(op, n_vec), op.shape)
+        if planes:
+            sl = NumpyPlaneSlab(op, plan, rank, n_vec, DEG, True)
+            fill_plane_probes(sl, probes(op, n_vec))
+        else:
+            sl = NumpySlab(op, plan, rank, n_vec, DEG, True)
+            fill_probes(sl, probes(op, n_vec), op.shape)
         assert sl.parts  # 3 planes per slab: the boundary / interior split applies
         got = run_rowpartition([sl], plan, iv.center, iv.halfwidth, DEG, 1, group=None,
                                rank_of_slab=lambda s: s, overlap=overlap)
@@ -78,7 +82,8 @@ def _worker(rank, world, port, q, overlap):
 
 
 @pytest.mark.parametrize("overlap", [True, False])
-def test_two_rank_halo_exchange_gloo(overlap):
+@pytest.mark.parametrize("planes", [False, True], ids=["slab-blocks", "full-blocks"])
+def test_two_rank_halo_exchange_gloo(overlap, planes):
     import sys
 
     ctx = mp.get_context("spawn")
@@ -87,7 +92,7 @@ def test_two_rank_halo_exchange_gloo(overlap):
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     if root not in sys.path:
         sys.path.insert(0, root)
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, overlap)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, overlap, planes)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=180) for _ in procs)
@@ -99,3 +104,24 @@ def test_two_rank_halo_exchange_gloo(overlap):
     for r in (0, 1):
         assert np.max(np.abs(res[r] - ref)) <= 1e-11 * np.max(np.abs(ref))
     np.testing.assert_array_equal(res[0], res[1])
+
+
+@pytest.mark.parametrize("n_slabs", [1, 2, 3, 5])
+@pytest.mark.parametrize("doubling", [True, False])
+@pytest.mark.parametrize("overlap", [True, False])
+def test_single_process_full_blocks(n_slabs, doubling, overlap):
+    """The plane-range driver (PlaneSlab layout: full-size blocks, global plane
+    indices in the exchange) with NaN outside what each slab may read."""
+    from tests.slab_reference import NumpyPlaneSlab, fill_plane_probes
+
+    op = W.stencil27_3d(6) if n_slabs % 2 else W.anderson_3d(7)
+    n_vec = 3
+    ref, iv = reference(op, n_vec, doubling)
+    plan = SlabPlan(op.shape[2], n_slabs)
+    pr = probes(op, n_vec)
+    slabs = [NumpyPlaneSlab(op, plan, s, n_vec, DEG, doubling) for s in range(n_slabs)]
+    for sl in slabs:
+        fill_plane_probes(sl, pr)
+    got = run_rowpartition(slabs, plan, iv.center, iv.halfwidth, DEG, 1 if doubling else 0, overlap=overlap).numpy()
+    assert np.all(np.isfinite(got))
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(ref))

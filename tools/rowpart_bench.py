@@ -56,10 +56,11 @@ def main():
         slabs.append(sl)
     c, d = float(iv.center), float(iv.halfwidth)
     res["p2p"] = timed(lambda: RP.run_rowpartition_p2p(slabs, plan, c, d, args.degree, mode))
-    for sl in slabs:
-        sl.split_used = False
     res["copy"] = timed(lambda: RP.run_rowpartition(slabs, plan, c, d, args.degree, mode, overlap=False))
     res["copy+split"] = timed(lambda: RP.run_rowpartition(slabs, plan, c, d, args.degree, mode, overlap=True))
+    pslabs = [RP.make_slab(op, plan, s, args.n_vec, args.degree, mode, 0, src, True) for s in range(args.slabs)]
+    res["planes"] = timed(lambda: RP.run_rowpartition(pslabs, plan, c, d, args.degree, mode, overlap=False))
+    res["planes+split"] = timed(lambda: RP.run_rowpartition(pslabs, plan, c, d, args.degree, mode, overlap=True))
     print({k: round(v, 3) for k, v in res.items()}, f"ms/step (n={args.n}^3, {args.slabs} slabs, "
           f"{args.n_vec} probes; 'whole' includes its probe draw)")
 
