@@ -207,6 +207,15 @@ SDB_API int sdb_cheb_step_planes(const sdb_matrix* m, double c, double d, int64_
                                  int64_t k, int64_t z_lo, int64_t z_hi, const double* x, const double* prev,
                                  double* next, const double* v0, double* partials, size_t partial_bytes,
                                  void* stream);
+/* sdb_cheb_step_planes that also pushes the halo from the kernel epilogue:
+ * plane z_lo of w_{k+1} is stored at the same offset into halo_lo (the lower
+ * neighbour slab's full-size `next` block; peer device memory over NVLink or
+ * this device), plane z_hi-1 into halo_hi; either may be NULL.  The caller
+ * orders step k+1 of a slab after its neighbours' step k. */
+SDB_API int sdb_cheb_step_planes_halo(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree,
+                                      int mode, int64_t k, int64_t z_lo, int64_t z_hi, const double* x,
+                                      const double* prev, double* next, const double* v0, double* partials,
+                                      size_t partial_bytes, double* halo_lo, double* halo_hi, void* stream);
 SDB_API int sdb_cheb_reduce_planes(const sdb_matrix* m, int64_t n_vec, int64_t degree, int mode, int64_t z_lo,
                                    int64_t z_hi, const double* partials, double* zeta_pp, void* stream);
 /* zeta[k] = (1/n_vec) sum_l zeta_pp[l][k], probes summed in index order

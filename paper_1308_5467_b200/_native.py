@@ -96,6 +96,8 @@ SIGNATURES = {
     "sdb_zm_block_info": (_i, [_p, _i64, _i, ctypes.POINTER(_i64), ctypes.POINTER(_sz)]),
     "sdb_zm_pad_probes": (_i, [_p, _i64, _p, _p, _p]),
     "sdb_cheb_step_planes": (_i, [_p, _d, _d, _i64, _i64, _i, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p]),
+    "sdb_cheb_step_planes_halo": (_i, [_p, _d, _d, _i64, _i64, _i, _i64, _i64, _i64, _p, _p, _p, _p, _p, _sz, _p, _p,
+                                       _p]),
     "sdb_cheb_reduce_planes": (_i, [_p, _i64, _i64, _i, _i64, _i64, _p, _p, _p]),
     "sdb_enable_peer_access": (_i, [_i, _i]),
     "sdb_cheb_reduce": (_i, [_p, _i64, _i64, _i, _p, _p, _p]),

@@ -1008,9 +1008,30 @@ int sdb_zm_pad_probes(const sdb_matrix* m, int64_t n_vec, const double* probes, 
   return zm_pad(m, zp, probes, ldv, padded, (cudaStream_t)stream);
 }
 
+static int step_planes_impl(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode,
+                            int64_t k, int64_t z_lo, int64_t z_hi, const double* x, const double* prev, double* next,
+                            const double* v0, double* partials, size_t partial_bytes, double* halo_lo,
+                            double* halo_hi, void* stream);
+
 int sdb_cheb_step_planes(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode, int64_t k,
                          int64_t z_lo, int64_t z_hi, const double* x, const double* prev, double* next,
                          const double* v0, double* partials, size_t partial_bytes, void* stream) {
+  return step_planes_impl(m, c, d, n_vec, degree, mode, k, z_lo, z_hi, x, prev, next, v0, partials, partial_bytes,
+                          nullptr, nullptr, stream);
+}
+
+int sdb_cheb_step_planes_halo(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode,
+                              int64_t k, int64_t z_lo, int64_t z_hi, const double* x, const double* prev,
+                              double* next, const double* v0, double* partials, size_t partial_bytes,
+                              double* halo_lo, double* halo_hi, void* stream) {
+  return step_planes_impl(m, c, d, n_vec, degree, mode, k, z_lo, z_hi, x, prev, next, v0, partials, partial_bytes,
+                          halo_lo, halo_hi, stream);
+}
+
+static int step_planes_impl(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t degree, int mode,
+                            int64_t k, int64_t z_lo, int64_t z_hi, const double* x, const double* prev, double* next,
+                            const double* v0, double* partials, size_t partial_bytes, double* halo_lo,
+                            double* halo_hi, void* stream) {
   SDB_REQUIRE(m && x && next && partials, "NULL argument");
   int legendre;
   mode = split_mode(mode, &legendre);
@@ -1037,6 +1058,8 @@ int sdb_cheb_step_planes(const sdb_matrix* m, double c, double d, int64_t n_vec,
   a.x = x;
   a.prev = prev;
   a.next = next;
+  a.halo_lo = halo_lo;
+  a.halo_hi = halo_hi;
   a.slot0 = (k == 0) ? 0 : -1;
   set_step_scalars(a, k);
   if (mode == SDB_CHEB_DOUBLING) {

@@ -160,7 +160,7 @@ struct ZmMaps {
   CUtensorMap x, prev, v0, diag;
 };
 
-template <int SHAPE, int CS, int TX, int TY, int PPT, int MODE, bool FIRST>
+template <int SHAPE, int CS, int TX, int TY, int PPT, int MODE, bool FIRST, bool PUSH>
 __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
     cheb_step_zmarch(const __grid_constant__ ZmMaps maps, ZmArgs t, StepArgs a) {
   using G = GridShape<SHAPE>;
@@ -310,6 +310,17 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
           double* dst = pn + cofs[k];
           st_d2_cs(dst, wn);
           zm_store_ghosted(dst, wn, cx[k], cy[k], nx, ny, a.ldv, pstride_y, t.G);
+          // plane-range push (row partition, sdb_cheb_step_planes_halo): the
+          // first / last plane of the range also lands at the same offset in
+          // the neighbour slab's full-size block (peer memory over NVLink)
+          // (a separate instantiation: the extra address registers cost the
+          // plain step ~10 %, measured)
+          if constexpr (PUSH) {
+            if (a.halo_lo && p - 1 == t.z_lo)
+              zm_store_ghosted(a.halo_lo + (dst - a.next), wn, cx[k], cy[k], nx, ny, a.ldv, pstride_y, t.G);
+            if (a.halo_hi && p - 1 == t.z_hi - 1)
+              zm_store_ghosted(a.halo_hi + (dst - a.next), wn, cx[k], cy[k], nx, ny, a.ldv, pstride_y, t.G);
+          }
           if (MODE == SDB_CHEB_DOUBLING) {
             accA.x += wn.x * wn.x;
             accA.y += wn.y * wn.y;
@@ -740,23 +751,25 @@ static int zm_env(const char* name, int dflt) {
 }
 
 template <int SHAPE, int CFG, int MODE, bool FIRST>
-static const void* zm_kernel() {
+static const void* zm_kernel(bool push) {
   constexpr ZmCfg c = kZmCfgs[CFG];
-  return (const void*)cheb_step_zmarch<SHAPE, c.CS, c.TX, c.TY, c.PPT, MODE, FIRST>;
+  return push ? (const void*)cheb_step_zmarch<SHAPE, c.CS, c.TX, c.TY, c.PPT, MODE, FIRST, true>
+              : (const void*)cheb_step_zmarch<SHAPE, c.CS, c.TX, c.TY, c.PPT, MODE, FIRST, false>;
 }
 
 template <int SHAPE, int CFG>
-static const void* zm_kernel_rt(int mode, bool first) {
+static const void* zm_kernel_rt(int mode, bool first, bool push) {
   if (mode == SDB_CHEB_DOUBLING)
-    return first ? zm_kernel<SHAPE, CFG, SDB_CHEB_DOUBLING, true>() : zm_kernel<SHAPE, CFG, SDB_CHEB_DOUBLING, false>();
-  return first ? zm_kernel<SHAPE, CFG, SDB_CHEB_DIRECT, true>() : zm_kernel<SHAPE, CFG, SDB_CHEB_DIRECT, false>();
+    return first ? zm_kernel<SHAPE, CFG, SDB_CHEB_DOUBLING, true>(push)
+                 : zm_kernel<SHAPE, CFG, SDB_CHEB_DOUBLING, false>(push);
+  return first ? zm_kernel<SHAPE, CFG, SDB_CHEB_DIRECT, true>(push) : zm_kernel<SHAPE, CFG, SDB_CHEB_DIRECT, false>(push);
 }
 
-static const void* zm_kernel_for(int shape, int cfg, int mode, bool first) {
+static const void* zm_kernel_for(int shape, int cfg, int mode, bool first, bool push) {
 #define SDB_ZM_CFG_CASE(C)                                                                      \
   case C:                                                                                       \
-    return shape == SDB_SHAPE_FACE7 ? zm_kernel_rt<SDB_SHAPE_FACE7, C>(mode, first)             \
-                                    : zm_kernel_rt<SDB_SHAPE_BOX27, C>(mode, first);
+    return shape == SDB_SHAPE_FACE7 ? zm_kernel_rt<SDB_SHAPE_FACE7, C>(mode, first, push)       \
+                                    : zm_kernel_rt<SDB_SHAPE_BOX27, C>(mode, first, push);
   switch (cfg) {
     SDB_ZM_CFG_CASE(0)
     SDB_ZM_CFG_CASE(1)
@@ -981,7 +994,7 @@ int zm_launch_step(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, bool
   for (int o = 0; o < 27; ++o) t.wc[o] = o < m->nterms ? m->term_w_host[o] : 0.0;
   StepArgs aa = a;
   aa.nblocks = p.nbp;
-  const void* fn = zm_kernel_for(m->shape, p.cfg, mode, first);
+  const void* fn = zm_kernel_for(m->shape, p.cfg, mode, first, a.halo_lo != nullptr || a.halo_hi != nullptr);
   if (!fn) return fail(SDB_EUNSUPPORTED, "no z-march kernel for configuration %d", p.cfg);
   size_t smem = (size_t)p.R * zm_slot_doubles(c, mode, first) * sizeof(double) + 2 * p.R * sizeof(uint64_t);
   const int nt = c.TX * c.TY * (c.CS / 2) / c.PPT;

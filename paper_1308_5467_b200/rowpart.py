@@ -255,6 +255,18 @@ class PlaneSlab:
         z_lo, z_hi = self.parts[name]
         self._step(name, z_lo, z_hi, k, c, d, cur, prev, nxt, v0)
 
+    def step_halo(self, k, c, d, cur, prev, nxt, v0, halo_lo, halo_hi):
+        """Step of the slab's planes whose z-march epilogue also stores its
+        first / last plane of w_{k+1} into the neighbours' full-size blocks
+        (``halo_lo`` / ``halo_hi``: tensors on this or a peer device, or None)."""
+        part = self.partials["all"]
+        z0, z1 = self.z0, self.z0 + self.nzl
+        _native.call("sdb_cheb_step_planes_halo", self.dm.handle, c, d, self.n_vec, self.degree, self.mode, k, z0,
+                     z1, E.ptr(cur), E.ptr(prev) if prev is not None else None, E.ptr(nxt), E.ptr(v0), E.ptr(part),
+                     part.numel() * 8, E.ptr(halo_lo) if halo_lo is not None else None,
+                     E.ptr(halo_hi) if halo_hi is not None else None, self.stream)
+        self.used.add(("all", z0, z1))
+
     def reduce(self):
         import torch
 
@@ -330,6 +342,10 @@ def run_rowpartition_p2p(slabs, plan, c, d, degree, mode):
         for b in devices:
             _native.call("sdb_enable_peer_access", a, b)
     multi = len(devices) > 1
+    full = hasattr(slabs[0], "plane_doubles")
+    for sl in slabs:
+        if full:
+            sl.used.clear()
     cur = {s: by_id[s].blocks[0] for s in by_id}
     prev = {s: None for s in by_id}
     done = {}
@@ -342,7 +358,10 @@ def run_rowpartition_p2p(slabs, plan, c, d, degree, mode):
             if multi and k > 0:
                 for nb in {lo, hi}:
                     sl.torch_stream.wait_event(done[nb])
-            if push:
+            if push and full:  # neighbours' full-size blocks, same global plane index
+                sl.step_halo(k, c, d, cur[s], prev[s], nxt[s], sl.blocks[0], nxt[lo] if lo != s else None,
+                             nxt[hi] if hi != s else None)
+            elif push:  # neighbours' ghost planes
                 sl.step_halo(k, c, d, cur[s], prev[s], nxt[s], sl.blocks[0], nxt[lo][-1], nxt[hi][0])
             else:
                 sl.step(k, c, d, cur[s], prev[s], nxt[s], sl.blocks[0])
@@ -494,10 +513,10 @@ def rowpartition_moments(op, interval, degree, source, n_vec, mode=_native.SDB_C
     if min(plan.planes(s)[1] for s in range(plan.n_slabs)) < 1:
         raise ValueError("more slabs than z-planes")
     devs = [device] if (devices is None or rank_of_slab is not None) else [int(x) for x in devices]
-    use_planes = layout == "planes" or (layout == "auto" and (exchange != "p2p" or rank_of_slab is not None))
+    use_planes = layout in ("planes", "auto")
     slabs = [make_slab(op, plan, s, n_vec, degree, mode, devs[s % len(devs)], source, use_planes) for s in local]
     with torch.cuda.device(device):
-        if rank_of_slab is None and exchange == "p2p" and not hasattr(slabs[0], "plane_doubles"):
+        if rank_of_slab is None and exchange == "p2p":
             return run_rowpartition_p2p(slabs, plan, c, d, degree, mode)
         if overlap is None:
             overlap = rank_of_slab is not None

@@ -55,6 +55,9 @@ def test_p2p_devices_list_single_gpu():
     iv = W.gershgorin_interval(op)
     src = sdb.ProbeVectorSource("rademacher", seed=1, dim=op.dim)
     a = rowpartition_moments(op, iv, 21, src, 16, n_slabs=3, devices=[0, 0]).cpu().numpy()
+    b = rowpartition_moments(op, iv, 21, src, 16, n_slabs=3, exchange="copy").cpu().numpy()
+    np.testing.assert_array_equal(a, b)
+    a = rowpartition_moments(op, iv, 21, src, 16, n_slabs=3, devices=[0, 0], layout="slabs").cpu().numpy()
     b = rowpartition_moments(op, iv, 21, src, 16, n_slabs=3, exchange="copy", layout="slabs").cpu().numpy()
     np.testing.assert_array_equal(a, b)
 
@@ -77,7 +80,7 @@ def test_boundary_interior_split_matches_whole_slab_steps(mode):
 @pytest.mark.parametrize("builder", [lambda: W.anderson_3d(16), lambda: W.stencil27_3d(16)], ids=["face7", "box27"])
 @pytest.mark.parametrize("n_slabs", [1, 2, 3, 4])
 @pytest.mark.parametrize("mode", [1, 0], ids=["doubling", "direct"])
-@pytest.mark.parametrize("overlap", [True, False])
+@pytest.mark.parametrize("overlap", [True, False, "p2p"])
 def test_plane_range_zmarch_slabs(builder, n_slabs, mode, overlap):
     """Row partition on full-size z-march blocks (sdb_cheb_step_planes): each
     slab computes its planes with the TMA z-march kernel; planes it does not
@@ -89,8 +92,12 @@ def test_plane_range_zmarch_slabs(builder, n_slabs, mode, overlap):
     src = sdb.ProbeVectorSource("rademacher", seed=6, dim=op.dim)
     plan = RP.SlabPlan(op.shape[2], n_slabs)
     assert isinstance(RP.make_slab(op, plan, 0, 32, 31, mode, 0, src, True), RP.PlaneSlab)
-    got = rowpartition_moments(op, iv, 31, src, 32, mode=mode, n_slabs=n_slabs, exchange="copy", overlap=overlap,
-                               layout="planes").cpu().numpy()
+    if overlap == "p2p":  # halo pushed by the z-march epilogue into the neighbours' blocks
+        got = rowpartition_moments(op, iv, 31, src, 32, mode=mode, n_slabs=n_slabs, exchange="p2p",
+                                   layout="planes").cpu().numpy()
+    else:
+        got = rowpartition_moments(op, iv, 31, src, 32, mode=mode, n_slabs=n_slabs, exchange="copy",
+                                   overlap=overlap, layout="planes").cpu().numpy()
     ref = O.chebyshev_moments(op.csr, iv.center, iv.halfwidth, 31, "rademacher", 6, 32, mode="direct")
     assert np.all(np.isfinite(got))
     assert np.max(np.abs(got - ref)) <= 1e-10 * np.max(np.abs(ref))

@@ -61,6 +61,7 @@ def main():
     pslabs = [RP.make_slab(op, plan, s, args.n_vec, args.degree, mode, 0, src, True) for s in range(args.slabs)]
     res["planes"] = timed(lambda: RP.run_rowpartition(pslabs, plan, c, d, args.degree, mode, overlap=False))
     res["planes+split"] = timed(lambda: RP.run_rowpartition(pslabs, plan, c, d, args.degree, mode, overlap=True))
+    res["planes+p2p"] = timed(lambda: RP.run_rowpartition_p2p(pslabs, plan, c, d, args.degree, mode))
     print({k: round(v, 3) for k, v in res.items()}, f"ms/step (n={args.n}^3, {args.slabs} slabs, "
           f"{args.n_vec} probes; 'whole' includes its probe draw)")
 
