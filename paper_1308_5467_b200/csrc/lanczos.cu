@@ -302,7 +302,8 @@ constexpr int kZcs = 16;
 
 template <int KMAX, int kZrows, int kZtg>
 __global__ void __launch_bounds__(kZcs * kZtg, (KMAX * kZrows * kZtg >= 256) ? 1 : 2)
-    lz_update_proj(const double* __restrict__ basis, double* __restrict__ w, const double* __restrict__ h, int64_t j,
+    lz_update_proj(const double* __restrict__ basis, const double* __restrict__ wsrc, double* __restrict__ w,
+                   const double* __restrict__ h, int64_t j,
                    int64_t n, int64_t ldv, int64_t nrb, double* __restrict__ partials) {
   const int c = threadIdx.x % kZcs, tg = threadIdx.x / kZcs;
   const int64_t rb = blockIdx.y;  // column slices of the same rows run side by side
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(kZcs * kZtg, (KMAX * kZrows * kZtg >= 256) ? 1
     double2 v[kZrows][KMAX];
     double2 wv = make_double2(0.0, 0.0);
     const bool wown = tg < kZrows && colok && r0 + tg < re;
-    if (wown) wv = ld_d2(w + (r0 + tg) * ldv + col);  // in flight with the basis loads
+    if (wown) wv = ld_d2(wsrc + (r0 + tg) * ldv + col);  // in flight with the basis loads
 #pragma unroll
     for (int r = 0; r < kZrows; ++r)
 #pragma unroll
@@ -520,7 +521,8 @@ static int lz_launch_update(const Geometry& g, bool norm, const double* basis, d
 
 // Fused middle pass when the per-thread t range fits the register budget.
 template <int KM, int RW, int TG>
-static void lz_upj_launch(dim3 grid, const double* basis, double* w, const double* h, int64_t j, int64_t n,
+static void lz_upj_launch(dim3 grid, const double* basis, const double* wsrc, double* w, const double* h, int64_t j,
+                          int64_t n,
                           int64_t ldv, int64_t nrb, double* part, cudaStream_t s) {
   const size_t smem = (size_t)KM * TG * kZcs * sizeof(double2);
   static bool attr = false;
@@ -528,16 +530,17 @@ static void lz_upj_launch(dim3 grid, const double* basis, double* w, const doubl
     cudaFuncSetAttribute(lz_update_proj<KM, RW, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  lz_update_proj<KM, RW, TG><<<grid, kZcs * TG, smem, s>>>(basis, w, h, j, n, ldv, nrb, part);
+  lz_update_proj<KM, RW, TG><<<grid, kZcs * TG, smem, s>>>(basis, wsrc, w, h, j, n, ldv, nrb, part);
 }
 
-static bool lz_launch_update_proj(const double* basis, double* w, const double* h, int64_t j, int64_t n, int64_t ldv,
+static bool lz_launch_update_proj(const double* basis, const double* wsrc, double* w, const double* h, int64_t j,
+                                  int64_t n, int64_t ldv,
                                   int64_t nrb, double* part, cudaStream_t s) {
   dim3 grid((unsigned)((ldv / 2 + kZcs - 1) / kZcs), (unsigned)nrb);
   const int64_t T = j + 1;
 #define SDB_UPJ(KM, RW, TG)                                                  \
   if (T <= (int64_t)KM * TG) {                                               \
-    lz_upj_launch<KM, RW, TG>(grid, basis, w, h, j, n, ldv, nrb, part, s);  \
+    lz_upj_launch<KM, RW, TG>(grid, basis, wsrc, w, h, j, n, ldv, nrb, part, s);  \
     return true;                                                             \
   }
   // two rows per iteration (measured best on C4: 16 t-groups x 2 rows beats
@@ -546,6 +549,8 @@ static bool lz_launch_update_proj(const double* basis, double* w, const double* 
 #undef SDB_UPJ
   return false;
 }
+
+static bool lz_update_proj_fits(int64_t j) { return j + 1 <= 16LL * 16; }
 
 static bool lz_fused_enabled() {
   const char* e = getenv("SDB_LZ_FUSED");
@@ -633,19 +638,31 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
     SDB_CHECK_LAUNCH();
     const int hblk = (int)(((j + 1) * ldv + 255) / 256);
     if (reorth == SDB_REORTH_FULL) {
-      // pass 1: w' = w - alpha v_j -> W0, h = V^T w'; w' -= V h
-      if ((rc = lz_launch_proj(nv, true, false, basis, W1, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
-      SDB_CHECK_LAUNCH();
-      lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
-      SDB_CHECK_LAUNCH();
-      // pass 2: h = V^T w; w -= V h; ||w||^2  (update of pass 1 + projection
-      // of pass 2 fused into one basis read when the t range fits registers)
-      if (!(fused && lz_launch_update_proj(basis, W0, h, j, n, ldv, nrb, part, s))) {
+      // pass 1 + 2.  Fused schedule (3 basis reads): h1 = V^T w on the raw w
+      // (v_j is a basis column, so CGS on w also removes alpha v_j: the
+      // reference's explicit w -= alpha v_j (lanczos.py:101-102) folds into
+      // h1[j]); then w' = w - V h1 -> W0 together with h2 = V^T w' (K5c);
+      // then w' -= V h2 with ||w'||^2.  Fallback (t range beyond the fused
+      // kernel's registers): the reference order with 4 basis reads.
+      const bool fz = fused && lz_update_proj_fits(j);
+      if (fz) {
+        if ((rc = lz_launch_proj(nv, false, false, basis, W1, W1, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
+        SDB_CHECK_LAUNCH();
+        lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
+        SDB_CHECK_LAUNCH();
+        lz_launch_update_proj(basis, W1, W0, h, j, n, ldv, nrb, part, s);
+        SDB_CHECK_LAUNCH();
+      } else {
+        // w' = w - alpha v_j -> W0, h = V^T w'; w' -= V h; h = V^T w'
+        if ((rc = lz_launch_proj(nv, true, false, basis, W1, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
+        SDB_CHECK_LAUNCH();
+        lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
+        SDB_CHECK_LAUNCH();
         if ((rc = lz_launch_update(g, false, basis, W0, h, j, n, nrb, panel, part, s))) return rc;
         SDB_CHECK_LAUNCH();
         if ((rc = lz_launch_proj(nv, false, false, basis, W0, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
+        SDB_CHECK_LAUNCH();
       }
-      SDB_CHECK_LAUNCH();
       lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
       SDB_CHECK_LAUNCH();
       if ((rc = lz_launch_update(g, true, basis, W0, h, j, n, nrb, panel, part, s))) return rc;

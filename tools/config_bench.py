@@ -73,11 +73,16 @@ def main():
 
             ma = device_matrix(res.base, dev, E.stream_ptr(dev)).bytes_per_pass
             m = cfg.degree
-            total = sum(ma + 8 * n * ldv * (4 * (j + 1) + 11) for j in range(m))
+            # traffic of the schedule that ran: fused (default, <= 256 steps):
+            # SpMM 4 passes + proj (V, w) + K5c (V, w in, w out) + update (V, w rmw);
+            # SDB_LZ_FUSED=0: the 4-pass reference order
+            fused = os.environ.get("SDB_LZ_FUSED", "1") != "0" and m <= 256
+            total = sum(ma + 8 * n * ldv * ((3 * (j + 1) + 9) if fused else (4 * (j + 1) + 11)) for j in range(m))
             minimal = sum(ma + 8 * n * ldv * (3 * (j + 1) + 3) for j in range(m))
             t = statistics.median(times)
             out = {"config": name, "method": "lanczos", "n": n, "nnz": nnz, "n_vec": cfg.n_vec, "steps": m,
                    "seconds": t, "gnnz_vec_s": nnz * cfg.n_vec * m / t / 1e9,
+                   "schedule": "fused CGS2 (3 basis reads)" if fused else "4-pass CGS2",
                    "bytes_moved_model_TB": total / 1e12, "achieved_GBs": total / t / 1e9,
                    "frac_of_peak": total / t / 1e9 / peak, "minimal_3pass_TB": minimal / 1e12,
                    "frac_vs_minimal_bytes": minimal / t / 1e9 / peak, "gen_s": gen_s}
