@@ -308,8 +308,7 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
               wn = make_double2(2.0 * tx - wp.x, 2.0 * ty - wp.y);
           }
           double* dst = pn + cofs[k];
-          st_d2_cs(dst, wn);
-          zm_store_ghosted(dst, wn, cx[k], cy[k], nx, ny, a.ldv, pstride_y, t.G);
+          zm_store_ghosted(dst, wn, cx[k], cy[k], nx, ny, a.ldv, pstride_y, t.G);  // point + its ghost images
           // plane-range push (row partition, sdb_cheb_step_planes_halo): the
           // first / last plane of the range also lands at the same offset in
           // the neighbour slab's full-size block (peer memory over NVLink)
