@@ -861,7 +861,10 @@ int zm_plan_range(const sdb_matrix* m, int64_t ldv, int mode, int64_t z_lo, int6
   p.TX = c.TX;
   p.TY = c.TY;
   const int slices = (int)(ldv / c.CS);
-  // ring depth from the largest slot (direct mode after the first step)
+  // ring depth from the largest slot (direct mode after the first step): 7 for
+  // the 16-column 8x8 tiles.  Measured (C2 doubling, whose slots would allow
+  // 10): R = 6 / 7 / 8 / 10 -> 71.3 / 69.9 / 74.8 / 82.2 us per step -- deeper
+  // prefetch runs the TMA further ahead of the neighbouring tiles and loses
   const int64_t slot_max = zm_slot_doubles(c, SDB_CHEB_DIRECT, false);
   const size_t budget = 220 * 1024;
   int R = (int)((budget - 256) / (slot_max * sizeof(double)));
