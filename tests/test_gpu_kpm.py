@@ -340,3 +340,36 @@ def test_rademacher_sign_staging_is_exact():
     a = sdb.moments_via_product_formula(mapped, 40, src, 33)
     b = sdb.moments_via_product_formula(mapped, 40, PlainSource(src), 33)
     np.testing.assert_array_equal(a.zeta, b.zeta)
+
+
+@pytest.mark.parametrize("n_vec", [1, 20, 130])
+@pytest.mark.parametrize("pf", [False, True])
+def test_csr_with_empty_rows_and_unsorted_entries(n_vec, pf):
+    """Rows with no stored entries (zero rows/columns) and rows whose entries are
+    not column-sorted: the kernels sum each row in storage order (csr_matvec),
+    an empty row contributes -c x / d only."""
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(11)
+    n = 500
+    a = sp.random(n, n, density=0.01, random_state=3, format="csr")
+    a = a + a.T
+    dead = rng.choice(n, 60, replace=False)
+    keep = np.ones(n)
+    keep[dead] = 0.0
+    d = sp.diags(keep)
+    a = (d @ a @ d).tocsr()
+    a.eliminate_zeros()
+    assert np.sum(np.diff(a.indptr) == 0) >= 60
+    coo = a.tocoo()
+    order = rng.permutation(coo.nnz)  # storage order within rows becomes arbitrary
+    a = sp.csr_array((coo.data[order], (coo.row[order], coo.col[order])), shape=(n, n))
+    a.has_sorted_indices = False
+    mat = sdb.SparseSymmetricMatrix(csr=a)
+    iv = W.gershgorin_interval(mat)
+    src = sdb.ProbeVectorSource("gaussian", seed=5, dim=n)
+    fn = sdb.moments_via_product_formula if pf else sdb.compute_chebyshev_moments
+    got = fn(sdb.apply_spectral_map(mat, iv), 33, src, n_vec).zeta
+    per = O.chebyshev_moments(mat.csr, iv.center, iv.halfwidth, 33, "gaussian", 5, n_vec,
+                              mode="product" if pf else "direct")
+    assert rel_err(got, O.average_moments(per)) <= MOMENT_RTOL
