@@ -131,3 +131,222 @@ def estimate_dos(matrix, interval, method, degree, source, n_vec, sigma=None, et
     if product_formula:
         est.params["product_formula"] = True
     return est
+
+
+# ---------------------------------------------------------------------------
+# Repeated method x degree sweep (compare.py:144-284), SURVEY §8(f)-4.
+#
+# The device does the sweep's work in three batched passes instead of
+# reps x n_vec independent runs: the probes of every repetition (stream = rep)
+# are drawn on the host exactly as the reference draws them and stacked into
+# one device block, then ONE Chebyshev, ONE Legendre and ONE batched Lanczos
+# run cover all reps x n_vec recurrences at the largest degree; each rep's
+# moments are its probe-ordered mean of that run, every smaller degree is an
+# exact prefix (kpm.py:49-59, lanczos.py:134-149).  Per degree, the Ritz
+# quadratures of all probes come from one QL launch, pooled and blurred per
+# rep; Haydock evaluates each rep's prefix tridiagonals in one launch.  The
+# scoring references (the blurred exact spectrum on the two grids and at the
+# sup-Gaussian centres) are computed once, and the per-estimate errors stay on
+# the device until one read at the end.
+
+from dataclasses import dataclass, field  # noqa: E402
+
+from .density import RegularizationKernel  # noqa: E402
+from .kpm import MomentSequence  # noqa: E402
+from .lanczos import _blur_device, _pool_device, _ritz_device, lanczos_tridiagonals_device  # noqa: E402
+from .metrics import DEFAULT_SUP_CENTERS, check_sup_gaussian_grid, sup_gaussian_device  # noqa: E402
+from .operators import estimate_spectral_interval, resolve  # noqa: E402
+from .reference import blurred_spectrum_device, dense_eigensolve  # noqa: E402
+from .stochastic import ProbeVectorSource, draw_block  # noqa: E402
+
+# scored with the sup-Gaussian metric (their output approximates the raw spike
+# density); the rest are compared pointwise to the matching blur (compare.py:67-69)
+SPIKE_ESTIMATORS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb", "kpml", "cdos")
+
+
+@dataclass
+class MethodComparisonRow:
+    """Aggregated accuracy of one method at one degree across repetitions (compare.py:144-154)."""
+
+    method: str
+    degree: int
+    matvec_count: int
+    error_mean: float
+    error_std: float
+    mass_mean: float
+    errors: np.ndarray = field(repr=False, default=None)
+
+
+def _stacked_probes(kind, seed, dim, reps, n_vec, device):
+    """(reps*n_vec, dim) device block: rep r's probes are ProbeVectorSource(kind, seed, dim, stream=r)."""
+    torch = E._torch()
+    out = torch.empty((reps * n_vec, dim), dtype=torch.float64, device=device)
+    for rep in range(reps):
+        blk = draw_block(ProbeVectorSource(kind, seed, dim, stream=rep), 0, n_vec)
+        out[rep * n_vec:(rep + 1) * n_vec].copy_(torch.as_tensor(np.asarray(blk, dtype=np.float64)))
+    return out
+
+
+def _rep_moments(mapped, m_max, probes, reps, n_vec, mode, basis, device):
+    """One moment run over every rep's probes; each rep's probe-ordered mean as a MomentSequence."""
+    torch = E._torch()
+    run = E.run_chebyshev(mapped, m_max, None, reps * n_vec, mode, device=device, probes=probes)
+    means, flags = [], []
+    for rep in range(reps):
+        z, f = E.mean_moments(run.zeta_pp[rep * n_vec:(rep + 1) * n_vec], device)
+        means.append(z)
+        flags.append(f)
+    zeta = torch.stack(means).cpu().numpy()
+    if int(torch.cat(flags).max().item()) != 0 or not np.all(np.isfinite(zeta)):
+        raise NumericalFailure(E.SPECTRUM_ESCAPE_HINT)
+    return [MomentSequence(zeta=zeta[rep], degree=m_max, n_vec=n_vec, basis=basis, n=run.n) for rep in range(reps)]
+
+
+def run_method_comparison(matrix, methods, degrees, sigma, eta=None, n_vec=100, reps=10, seed=0,
+                          probe_kind="gaussian", grid_points=512, threads=None, interval=None, spectrum=None,
+                          device=None):
+    """Repeat a method x degree sweep and aggregate errors and masses (compare.py:162-284).
+
+    Same arguments, validation order, common random numbers (probe stream =
+    repetition), exact-prefix slicing, scoring protocol and rows as the
+    reference.  ``cdos`` (the monotone-spline refinement) is outside the
+    accelerated path and raises ``NotImplementedError``; ``threads`` is ignored.
+    """
+    for m in methods:
+        if m not in ALL_METHODS and m != "exact":
+            raise ValueError(f"unknown method {m!r}, expected one of {ALL_METHODS}")
+    if not sigma > 0:
+        raise ValueError("sigma must be positive")
+    degrees = sorted(set(int(m) for m in degrees))
+    if not degrees or degrees[0] < 1:
+        raise ValueError("degrees must be positive")
+    if "cdos" in methods:
+        raise NotImplementedError("method 'cdos' is outside the accelerated hot path")
+    torch = E._torch()
+    device = E.require_cuda(device)
+    op = as_operator(matrix)
+    if interval is None:
+        interval = estimate_spectral_interval(op, seed=seed, device=device)
+    if spectrum is None:
+        spectrum = dense_eigensolve(op, device=device)
+    if eta is None:
+        eta = sigma
+
+    m_max = degrees[-1]
+    unit_pts = unit_grid(grid_points)
+    lam_grid = interval_grid(interval, grid_points)
+    unit_lam = interval.from_unit(unit_pts)  # lambda_grid of the unit-grid estimates
+    gauss = RegularizationKernel("gaussian", sigma)
+
+    need_cheb = any(m in CHEBYSHEV_METHODS for m in methods)
+    need_leg = any(m in LEGENDRE_METHODS for m in methods)
+    need_lan = any(m in LANCZOS_METHODS for m in methods)
+    if any(m in SPIKE_ESTIMATORS for m in methods):
+        check_sup_gaussian_grid(unit_lam, sigma)
+
+    errors = {(m, deg): [] for m in methods for deg in degrees}
+    masses = {(m, deg): [] for m in methods for deg in degrees}
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        n = resolve(op).dim
+        probes = _stacked_probes(probe_kind, seed, n, reps, n_vec, device)
+        mapped = apply_spectral_map(op, interval)
+        cheb = (_rep_moments(mapped, m_max, probes, reps, n_vec, _native.SDB_CHEB_DIRECT, "chebyshev", device)
+                if need_cheb else None)
+        leg = (_rep_moments(mapped, m_max, probes, reps, n_vec, _native.SDB_LEGENDRE, "legendre", device)
+               if need_leg else None)
+        if need_lan:
+            steps = min(m_max, n)
+            _, alpha, beta, sd, st = lanczos_tridiagonals_device(op, steps, None, reps * n_vec, device=device,
+                                                                 probes=probes)
+
+        # scoring references, computed once
+        eig_dev = E.to_device(spectrum.eigenvalues, device)
+        lam_dev = E.to_device(lam_grid, device)
+        unit_lam_dev = E.to_device(unit_lam, device)
+        centers_dev = E.to_device(np.linspace(interval.lambda_lb, interval.lambda_ub, DEFAULT_SUP_CENTERS), device)
+        exact_centers = blurred_spectrum_device(spectrum, gauss, centers_dev, device, eig_dev)
+        exact_lam = blurred_spectrum_device(spectrum, gauss, lam_dev, device, eig_dev)
+        exact_unit = (blurred_spectrum_device(spectrum, gauss, unit_lam_dev, device, eig_dev)
+                      if "dgl" in methods else None)
+        exact_lam_h = exact_lam.cpu().numpy()
+
+        def score_spike(est):
+            return sup_gaussian_device(exact_centers, unit_lam_dev, E.to_device(est.density, device), centers_dev,
+                                       sigma, device)
+
+        def score_blur(density_dev, ref_dev):
+            return torch.max(torch.abs(density_dev - ref_dev))
+
+        for rep in range(reps):
+            sl = slice(rep * n_vec, (rep + 1) * n_vec)
+            for deg in degrees:
+                if need_lan:
+                    dp = min(deg, steps)
+                    a_p = alpha[:, :dp].contiguous()
+                    b_p = beta[:, :dp].contiguous()
+                    sd_p = torch.clamp(sd, max=dp).to(torch.int32)
+                    if "lanczos" in methods:
+                        th, tw = _ritz_device(a_p[sl], b_p[sl], sd_p[sl], dp, device, stream)
+                        nodes, weights = _pool_device(th, tw, sd_p[sl], n_vec, device, stream)
+                        lan_dens = _blur_device(nodes, weights, lam_dev, "gaussian", sigma, 1.0, device, stream)
+                    if "haydock" in methods:
+                        hay_dens = torch.empty_like(lam_dev)
+                        _native.call("sdb_haydock", E.ptr(a_p[sl]), E.ptr(b_p[sl]), E.ptr(sd_p[sl]), E.ptr(st[sl]),
+                                     n_vec, dp, E.ptr(lam_dev), lam_dev.numel(), float(eta), E.ptr(hay_dens), None,
+                                     None, stream)
+                for method in methods:
+                    if method == "exact":
+                        # oracle scored against itself: a zero-error control row
+                        err = score_blur(exact_lam, exact_lam)
+                        mass = float(np.trapezoid(exact_lam_h, lam_grid))
+                    elif method in CHEBYSHEV_METHODS or method in LEGENDRE_METHODS:
+                        moments = (cheb if method in CHEBYSHEV_METHODS else leg)[rep].truncated(deg)
+                        if method == "kpm":
+                            est = K.evaluate_kpm_dos(K.moments_to_coefficients(moments, "none", device=device),
+                                                     interval, unit_pts, device=device)
+                        elif method == "kpm-jackson":
+                            est = K.evaluate_kpm_dos(K.moments_to_coefficients(moments, "jackson", device=device),
+                                                     interval, unit_pts, device=device)
+                        elif method == "spectroscopic":
+                            est = K.spectroscopic_dos(moments, interval, unit_pts, device=device)
+                        elif method == "delta-cheb":
+                            est = K.delta_chebyshev_dos(moments, interval, unit_pts, device=device)
+                        elif method == "kpml":
+                            est = K.evaluate_kpml_dos(moments, interval, unit_pts, device=device)
+                        else:
+                            est = evaluate_dgl_dos(moments, interval, sigma, unit_pts, device=device)
+                        if method in SPIKE_ESTIMATORS:
+                            err = score_spike(est)
+                        else:
+                            err = score_blur(E.to_device(est.density, device), exact_unit)
+                        mass = est.mass()
+                    else:
+                        dens = lan_dens if method == "lanczos" else hay_dens
+                        err = score_blur(dens, exact_lam)
+                        mass = float(np.trapezoid(dens.cpu().numpy(), lam_grid))
+                    errors[(method, deg)].append(err)
+                    masses[(method, deg)].append(mass)
+        keys = list(errors)
+        flat = torch.stack([e for k in keys for e in errors[k]]).cpu().numpy() if keys else np.zeros(0)
+
+    rows = []
+    pos = 0
+    per_key = {}
+    for k in keys:
+        per_key[k] = flat[pos:pos + len(errors[k])]
+        pos += len(errors[k])
+    for method in methods:
+        for deg in degrees:
+            errs = np.asarray(per_key[(method, deg)], dtype=float)
+            rows.append(MethodComparisonRow(
+                method=method,
+                degree=deg,
+                matvec_count=analytic_matvec_count(method, deg, n_vec),
+                error_mean=float(errs.mean()),
+                error_std=float(errs.std(ddof=1)) if reps > 1 else 0.0,
+                mass_mean=float(np.mean(masses[(method, deg)])),
+                errors=errs,
+            ))
+    return rows
+

@@ -181,3 +181,37 @@ def test_rademacher_sign_bits_round_trip():
         np.testing.assert_array_equal(v, src.draw(5 + i))
     with pytest.raises(ValueError):
         sdb.ProbeVectorSource("gaussian", 0, 10).draw_block_signs(0, 1)
+
+
+def test_comparison_validates_before_device_work():
+    """pkg/tests/test_compare.py:62-67, :106-112: argument errors come first (no GPU needed)."""
+    lap = W.generate_modified_laplacian_2d(10, 5)
+    with pytest.raises(ValueError, match="unknown method"):
+        sdb.run_method_comparison(lap, ["kpm", "kmp"], [10], sigma=0.4)
+    with pytest.raises(ValueError, match="sigma"):
+        sdb.run_method_comparison(lap, ["kpm"], [10], sigma=0.0)
+    with pytest.raises(ValueError, match="degrees"):
+        sdb.run_method_comparison(lap, ["kpm"], [], sigma=0.4)
+    with pytest.raises(ValueError, match="degrees"):
+        sdb.run_method_comparison(lap, ["kpm"], [0, 10], sigma=0.4)
+    with pytest.raises(NotImplementedError, match="cdos"):
+        sdb.run_method_comparison(lap, ["kpm", "cdos"], [10], sigma=0.4)
+
+
+def test_comparison_golden_rows_are_consistent():
+    """The reference's rows in the fixture: exact rows are zero, delta-cheb == kpm, means/std of the errors."""
+    import os
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "method_comparison.npz"))
+    for name in ("small_lap", "tiny_capped"):
+        p = name + "/"
+        methods = [str(m) for m in z[p + "row_method"]]
+        errs = z[p + "row_errors"]
+        np.testing.assert_allclose(errs.mean(axis=1), z[p + "row_mean"], rtol=1e-14)
+        np.testing.assert_allclose(errs.std(axis=1, ddof=1), z[p + "row_std"], rtol=1e-12)
+        for i, m in enumerate(methods):
+            if m == "exact":
+                assert np.all(errs[i] == 0.0)
+            if m == "delta-cheb":
+                j = [k for k, mm in enumerate(methods) if mm == "kpm" and z[p + "row_degree"][k] == z[p + "row_degree"][i]][0]
+                np.testing.assert_array_equal(errs[i], errs[j])
