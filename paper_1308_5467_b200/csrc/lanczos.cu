@@ -35,6 +35,36 @@ struct LzState {       // per-probe device state, each an ldv-long array
   double* alpha_cur;   // alpha_j
 };
 
+// Column sums of a [slot][nblocks][ldv] partials array, block-parallel in a
+// fixed order: the block is 32 columns x SEGS segments; segment k sums rows
+// k, k+SEGS, ... in order, then segment 0 adds the SEGS segment sums in order.
+// Deterministic (the same tree every launch).  The serial per-column loop it
+// replaces left ~ldv threads walking nblocks rows each (the reduce kernels ran
+// at a few hundred GB/s on 28 MB of partials late in a 100-step run).
+// Every thread of the block must call it; the result is valid for seg == 0.
+template <int SEGS>
+__device__ __forceinline__ double block_col_sum(const double* __restrict__ partials, int64_t slot, int64_t nblocks,
+                                                int64_t ldv, int64_t l) {
+  __shared__ double red[SEGS][32];
+  const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  double s = 0.0;
+  if (l < ldv) {
+    const double* p = partials + slot * nblocks * ldv + l;
+#pragma unroll 4
+    for (int64_t b = seg; b < nblocks; b += SEGS) s += p[b * ldv];
+  }
+  red[seg][lane] = s;
+  __syncthreads();
+  double tot = 0.0;
+  if (seg == 0) {
+#pragma unroll
+    for (int k = 0; k < SEGS; ++k) tot += red[k][lane];
+  }
+  __syncthreads();
+  return tot;
+}
+constexpr int kRedSegs = 16;
+
 // ---- start: ||v0|| --------------------------------------------------------------
 template <int L, int VPL>
 __global__ void __launch_bounds__(kRowThreads) lz_start_norm(const double* __restrict__ v0, int64_t n, int64_t ldv,
@@ -123,9 +153,9 @@ __global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
 __global__ void lz_alpha_reduce(const double* __restrict__ partials, int64_t nblocks, int64_t ldv, int64_t n_vec,
                                 int64_t j, int64_t steps, LzState st, double* __restrict__ alpha,
                                 const int32_t* __restrict__ status) {
-  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (l >= ldv) return;
-  const double a = sum_blocks(partials, 0, nblocks, ldv, l);
+  const int64_t l = blockIdx.x * 32 + (threadIdx.x & 31);
+  const double a = block_col_sum<kRedSegs>(partials, 0, nblocks, ldv, l);
+  if ((threadIdx.x >> 5) != 0 || l >= ldv) return;
   const bool live = l < n_vec && status[l] == SDB_LZ_OK;
   st.alpha_cur[l] = live ? a : 0.0;
   if (live) alpha[l * steps + j] = a;
@@ -208,17 +238,14 @@ __global__ void __launch_bounds__(kProjWarps * 32)
 // overlaps above sqrt(eps) ||w|| (lanczos.py:107-110).
 __global__ void lz_h_reduce(const double* __restrict__ partials, int64_t nrb, int64_t ldv, int64_t j,
                             double* __restrict__ h, int selective, int64_t norm_slot) {
-  const int64_t total = (j + 1) * ldv;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = idx / ldv, l = idx % ldv;
-    double v = sum_blocks(partials, t, nrb, ldv, l);
-    if (selective) {
-      const double wn = sqrt(sum_blocks(partials, norm_slot, nrb, ldv, l));
-      if (!(fabs(v) > 1.4901161193847656e-08 * wn)) v = 0.0;
-    }
-    h[idx] = v;
+  // grid (t, column chunk of 32); see block_col_sum
+  const int64_t t = blockIdx.x, l = blockIdx.y * 32 + (threadIdx.x & 31);
+  double v = block_col_sum<kRedSegs>(partials, t, nrb, ldv, l);
+  if (selective) {
+    const double wn = sqrt(block_col_sum<kRedSegs>(partials, norm_slot, nrb, ldv, l));
+    if (!(fabs(v) > 1.4901161193847656e-08 * wn)) v = 0.0;
   }
+  if ((threadIdx.x >> 5) == 0 && l < ldv) h[t * ldv + l] = v;
 }
 
 // ---- K5b: w -= V h (row-local), optional ||w||^2 partials ---------------------------
@@ -421,9 +448,9 @@ __global__ void __launch_bounds__(kRowThreads) lz_sub_alpha_norm(const double* _
 __global__ void lz_beta_reduce(const double* __restrict__ partials, int64_t nblocks, int64_t ldv, int64_t n_vec,
                                int64_t j, int64_t steps, LzState st, double* __restrict__ beta,
                                int32_t* __restrict__ steps_done, int32_t* __restrict__ status) {
-  const int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (l >= ldv) return;
-  const double b = sqrt(sum_blocks(partials, 0, nblocks, ldv, l));
+  const int64_t l = blockIdx.x * 32 + (threadIdx.x & 31);
+  const double b = sqrt(block_col_sum<kRedSegs>(partials, 0, nblocks, ldv, l));
+  if ((threadIdx.x >> 5) != 0 || l >= ldv) return;
   if (l >= n_vec || status[l] != SDB_LZ_OK) {
     st.inv_beta[l] = 0.0;
     st.beta_prev[l] = 0.0;
@@ -612,6 +639,7 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
   const int rblk = (int)((ldv + 127) / 128);
   lz_start_reduce<<<rblk, 128, 0, s>>>(part, nrb, ldv, n_vec, st, steps_done, status);
   SDB_CHECK_LAUNCH();
+  const int cblk = (int)((ldv + 31) / 32);
 
   StencilView sv{};
   CsrView cv{};
@@ -634,9 +662,9 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
       rc = lz_launch_spmm(sv, g, wraw, vprev, vj, W1, st, j == 0, c, 1.0 / d, n, nrb, panel, part, s);
     if (rc) return rc;
     SDB_CHECK_LAUNCH();
-    lz_alpha_reduce<<<rblk, 128, 0, s>>>(part, nrb, ldv, n_vec, j, steps, st, alpha, status);
+    lz_alpha_reduce<<<cblk, 32 * kRedSegs, 0, s>>>(part, nrb, ldv, n_vec, j, steps, st, alpha, status);
     SDB_CHECK_LAUNCH();
-    const int hblk = (int)(((j + 1) * ldv + 255) / 256);
+    const dim3 hblk((unsigned)(j + 1), (unsigned)cblk);
     if (reorth == SDB_REORTH_FULL) {
       // pass 1 + 2.  Fused schedule (3 basis reads): h1 = V^T w on the raw w
       // (v_j is a basis column, so CGS on w also removes alpha v_j: the
@@ -648,7 +676,7 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
       if (fz) {
         if ((rc = lz_launch_proj(nv, false, false, basis, W1, W1, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
         SDB_CHECK_LAUNCH();
-        lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
+        lz_h_reduce<<<hblk, 32 * kRedSegs, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
         SDB_CHECK_LAUNCH();
         lz_launch_update_proj(basis, W1, W0, h, j, n, ldv, nrb, part, s);
         SDB_CHECK_LAUNCH();
@@ -656,21 +684,21 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
         // w' = w - alpha v_j -> W0, h = V^T w'; w' -= V h; h = V^T w'
         if ((rc = lz_launch_proj(nv, true, false, basis, W1, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
         SDB_CHECK_LAUNCH();
-        lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
+        lz_h_reduce<<<hblk, 32 * kRedSegs, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
         SDB_CHECK_LAUNCH();
         if ((rc = lz_launch_update(g, false, basis, W0, h, j, n, nrb, panel, part, s))) return rc;
         SDB_CHECK_LAUNCH();
         if ((rc = lz_launch_proj(nv, false, false, basis, W0, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
         SDB_CHECK_LAUNCH();
       }
-      lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
+      lz_h_reduce<<<hblk, 32 * kRedSegs, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
       SDB_CHECK_LAUNCH();
       if ((rc = lz_launch_update(g, true, basis, W0, h, j, n, nrb, panel, part, s))) return rc;
       SDB_CHECK_LAUNCH();
     } else if (reorth == SDB_REORTH_SELECTIVE) {
       if ((rc = lz_launch_proj(nv, true, true, basis, W1, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
       SDB_CHECK_LAUNCH();
-      lz_h_reduce<<<hblk, 256, 0, s>>>(part, nrb, ldv, j, h, 1, norm_slot);
+      lz_h_reduce<<<hblk, 32 * kRedSegs, 0, s>>>(part, nrb, ldv, j, h, 1, norm_slot);
       SDB_CHECK_LAUNCH();
       if ((rc = lz_launch_update(g, true, basis, W0, h, j, n, nrb, panel, part, s))) return rc;
       SDB_CHECK_LAUNCH();
@@ -681,7 +709,7 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
 #undef SDB_NONE_CASE
       SDB_CHECK_LAUNCH();
     }
-    lz_beta_reduce<<<rblk, 128, 0, s>>>(part, nrb, ldv, n_vec, j, steps, st, beta, steps_done, status);
+    lz_beta_reduce<<<cblk, 32 * kRedSegs, 0, s>>>(part, nrb, ldv, n_vec, j, steps, st, beta, steps_done, status);
     SDB_CHECK_LAUNCH();
     wraw = W0;
   }
