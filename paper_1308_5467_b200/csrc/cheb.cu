@@ -152,6 +152,8 @@ __device__ __forceinline__ void gather_fma(const double* __restrict__ x, int64_t
 // storage order (csr_matvec order, matrix.py:101-102).
 template <int L, int VPL, int MODE, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_step_csr(CsrView A, StepArgs a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int RPW = 32 / L;
   constexpr int RPB = RPW * kStepWarps;
   constexpr int U = L < 4 ? L : (VPL == 1 ? SDB_U_V1 : (VPL == 2 ? SDB_U_V2 : 2));
@@ -209,6 +211,8 @@ __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_st
 // rows on a periodic face recompute wrapped coordinates.
 template <int L, int VPL, int MODE, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_step_stencil(StencilView S, StepArgs a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int RPW = 32 / L;
   constexpr int RPB = RPW * kStepWarps;
   constexpr int U = VPL == 1 ? 8 : (VPL == 2 ? 4 : 2);
@@ -281,6 +285,8 @@ inline GridShapeTable grid_shape_table(int shape) {
 
 template <int SHAPE, int L, int VPL, int MODE, bool FIRST>
 __global__ void __launch_bounds__(kStepThreads, step_min_blocks(L, VPL)) cheb_step_grid(StencilView S, StepArgs a0) {
+  pdl_wait();
+  pdl_trigger();
   using G = GridShape<SHAPE>;
   // column slices of one panel are adjacent blocks (slice fastest)
   const int slice = blockIdx.x % a0.slices;
@@ -447,24 +453,34 @@ template <int MODE, bool FIRST>
 static int launch_step(const sdb_matrix* m, const Geometry& g, const StencilView* st, const StepArgs& a,
                        cudaStream_t s) {
   dim3 grid((unsigned)(a.nblocks * a.slices)), block(kStepThreads);
+  cudaError_t err = cudaSuccess;
+  StepArgs aa = a;
   if (m->format == SDB_FMT_CSR) {
-    const CsrView A = make_csr_view(m);
-#define SDB_STEP_CASE(LL, VV) cheb_step_csr<LL, VV, MODE, FIRST><<<grid, block, 0, s>>>(A, a)
+    CsrView A = make_csr_view(m);
+    void* args[] = {(void*)&A, (void*)&aa};
+#define SDB_STEP_CASE(LL, VV) err = launch_maybe_pdl((const void*)cheb_step_csr<LL, VV, MODE, FIRST>, grid, block, args, 0, s)
     SDB_GEOMETRY_DISPATCH(g, SDB_STEP_CASE);
 #undef SDB_STEP_CASE
   } else if (m->shape == SDB_SHAPE_FACE7) {
-#define SDB_STEP_CASE(LL, VV) cheb_step_grid<SDB_SHAPE_FACE7, LL, VV, MODE, FIRST><<<grid, block, 0, s>>>(*st, a)
+    StencilView sv = *st;
+    void* args[] = {(void*)&sv, (void*)&aa};
+#define SDB_STEP_CASE(LL, VV) err = launch_maybe_pdl((const void*)cheb_step_grid<SDB_SHAPE_FACE7, LL, VV, MODE, FIRST>, grid, block, args, 0, s)
     SDB_GEOMETRY_DISPATCH(g, SDB_STEP_CASE);
 #undef SDB_STEP_CASE
   } else if (m->shape == SDB_SHAPE_BOX27) {
-#define SDB_STEP_CASE(LL, VV) cheb_step_grid<SDB_SHAPE_BOX27, LL, VV, MODE, FIRST><<<grid, block, 0, s>>>(*st, a)
+    StencilView sv = *st;
+    void* args[] = {(void*)&sv, (void*)&aa};
+#define SDB_STEP_CASE(LL, VV) err = launch_maybe_pdl((const void*)cheb_step_grid<SDB_SHAPE_BOX27, LL, VV, MODE, FIRST>, grid, block, args, 0, s)
     SDB_GEOMETRY_DISPATCH(g, SDB_STEP_CASE);
 #undef SDB_STEP_CASE
   } else {
-#define SDB_STEP_CASE(LL, VV) cheb_step_stencil<LL, VV, MODE, FIRST><<<grid, block, 0, s>>>(*st, a)
+    StencilView sv = *st;
+    void* args[] = {(void*)&sv, (void*)&aa};
+#define SDB_STEP_CASE(LL, VV) err = launch_maybe_pdl((const void*)cheb_step_stencil<LL, VV, MODE, FIRST>, grid, block, args, 0, s)
     SDB_GEOMETRY_DISPATCH(g, SDB_STEP_CASE);
 #undef SDB_STEP_CASE
   }
+  SDB_CUDA(err);
   return SDB_OK;
 }
 
@@ -610,7 +626,10 @@ static int launch_tile_t(const TilePlan& p, const StepArgs& a, cudaStream_t s) {
     configured = true;
   }
   dim3 grid((unsigned)(p.nblocks * p.slices));
-  fn<<<grid, kTileThreads, smem, s>>>(p.t, a);
+  TileArgs tt = p.t;
+  StepArgs aa = a;
+  void* args[] = {(void*)&tt, (void*)&aa};
+  SDB_CUDA(launch_maybe_pdl((const void*)fn, grid, dim3(kTileThreads), args, smem, s));
   return SDB_OK;
 }
 
@@ -817,6 +836,7 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
   double* diag_padded = zp.fuse ? (double*)((char*)workspace + 4 * blk) : nullptr;
   double* partials = (double*)((char*)workspace + (zp.fuse ? 4 * blk + zp.diag_bytes : (zp.on ? 3 : 2) * blk));
 
+  PdlScope pdl_scope;  // step kernels of this loop overlap their launch with the previous step's tail
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (step_ms) {
     SDB_CUDA(cudaEventCreate(&e0));

@@ -80,6 +80,27 @@ struct sdb_matrix {
 
 namespace sdb {
 
+// ---- programmatic dependent launch (PDL) between recurrence steps -----------
+// Inside sdb_cheb_moments every step kernel is launched with programmatic
+// stream serialisation: step k+1 is launched while step k runs, its blocks
+// take SMs as step k's blocks retire, and they wait in griddepcontrol.wait
+// until step k has completed and flushed.  So launch latency and block
+// start-up overlap the previous step's tail instead of sitting between the
+// steps.  Kernels launched without the attribute pass griddepcontrol.wait
+// immediately, so the same kernels serve every other entry point unchanged.
+// Every step kernel calls pdl_wait() before touching global memory.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Set for the duration of one sdb_cheb_moments step loop (thread-local): the
+// step launchers then add the PDL attribute.  SDB_PDL=0 disables it.
+struct PdlScope {
+  PdlScope();
+  ~PdlScope();
+};
+bool pdl_active();
+cudaError_t launch_maybe_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s);
+
 // Rows per panel of the phased-panel schedule (rowgroup.cuh) for a block
 // width of ldv doubles and RPB rows per block iteration.  SDB_PANEL_ROWS
 // overrides it (tuning).

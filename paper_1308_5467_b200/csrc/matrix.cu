@@ -51,6 +51,32 @@ int num_sms(int device) {
   return cache[device];
 }
 
+static thread_local int g_pdl_depth = 0;
+static bool pdl_env_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SDB_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+PdlScope::PdlScope() { ++g_pdl_depth; }
+PdlScope::~PdlScope() { --g_pdl_depth; }
+bool pdl_active() { return g_pdl_depth > 0 && pdl_env_enabled(); }
+
+cudaError_t launch_maybe_pdl(const void* fn, dim3 grid, dim3 block, void** args, size_t smem, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_active() ? 1 : 0;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 int64_t row_blocks(const sdb_matrix* m) {
   // 4 resident row-range blocks per SM; never fewer rows than one block
   // iteration per block for small matrices.

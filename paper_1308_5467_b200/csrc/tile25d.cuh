@@ -77,6 +77,8 @@ __global__ void __launch_bounds__(kTileThreads, 1) cheb_step_tile(TileArgs t, St
   double* planes = tsm;
   double* prevb = tsm + SM::R * SM::PLANE;
   double* diagb = prevb + SM::RP * SM::PREV;
+  pdl_wait();
+  pdl_trigger();
 
   // slice fastest: the CS-column slices of one tile run side by side, so each
   // x row is fetched from DRAM once and its other slices hit in L2

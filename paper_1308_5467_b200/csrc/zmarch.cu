@@ -143,6 +143,8 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
 
   const int nx = t.nx, ny = t.ny, nz = t.nz;
   const int64_t pstride_y = (int64_t)(nx + 2 * t.G) * a.ldv;  // padded row of points
@@ -395,6 +397,8 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
 
   const int nx = t.nx, ny = t.ny, nz = t.nz;
   const int64_t pstride_y = (int64_t)(nx + 2 * kZmGhost) * a.ldv;
@@ -961,7 +965,7 @@ int zm_launch_step(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, bool
     smem = (size_t)nt * 2 * sizeof(double) + 2 * p.R * sizeof(uint64_t);
   SDB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   void* args[] = {(void*)&maps, (void*)&t, (void*)&aa};
-  SDB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)p.grid), dim3(nt + 32), args, smem, s));
+  SDB_CUDA(launch_maybe_pdl(fn, dim3((unsigned)p.grid), dim3(nt + 32), args, smem, s));
   return SDB_OK;
 }
 
@@ -1021,7 +1025,7 @@ int zm_launch_pair(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, cons
   SDB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int nt = c.TX * c.TY * (c.CS / 2) / c.PPT;
   void* args[] = {(void*)&maps, (void*)&t, (void*)&aa};
-  SDB_CUDA(cudaLaunchKernel(fn, dim3((unsigned)p.grid), dim3(nt + 32), args, smem, s));
+  SDB_CUDA(launch_maybe_pdl(fn, dim3((unsigned)p.grid), dim3(nt + 32), args, smem, s));
   return SDB_OK;
 }
 
