@@ -27,6 +27,10 @@
 namespace sdb {
 
 constexpr int kProjWarps = 8;
+#ifndef SDB_PROJ_UNROLL
+#define SDB_PROJ_UNROLL 2
+#endif
+constexpr int kProjUnroll = SDB_PROJ_UNROLL;  // rows in flight per warp in lz_proj
 
 struct LzState {       // per-probe device state, each an ldv-long array
   double* inv_beta;    // 1/beta_{j-1} (0 once frozen)
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kProjWarps * 32)
   const bool active = t <= j;
   const bool storer = SUB_ALPHA && tchunk == 0 && warp == 0;
   if (active) {
-#pragma unroll 4
+#pragma unroll kProjUnroll
     for (int64_t i = rs; i < re; ++i) {
       const int64_t o = i * ldv + 2 * lane;
 #pragma unroll
