@@ -31,6 +31,10 @@ constexpr int kProjWarps = 8;
 #define SDB_PROJ_UNROLL 2
 #endif
 constexpr int kProjUnroll = SDB_PROJ_UNROLL;  // rows in flight per warp in lz_proj
+#ifndef SDB_UPD_TU
+#define SDB_UPD_TU 4
+#endif
+constexpr int kUpdTU = SDB_UPD_TU;  // basis vectors per load batch in lz_update
 
 struct LzState {       // per-probe device state, each an ldv-long array
   double* inv_beta;    // 1/beta_{j-1} (0 once frozen)
@@ -271,17 +275,17 @@ __global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
 #pragma unroll
       for (int v = 0; v < VPL; ++v) s[v] = make_double2(0.0, 0.0);
       int64_t t = 0;
-      for (; t + 4 <= j + 1; t += 4) {
-        double2 b[4][VPL], hh[4][VPL];
+      for (; t + kUpdTU <= j + 1; t += kUpdTU) {
+        double2 b[kUpdTU][VPL], hh[kUpdTU][VPL];
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kUpdTU; ++u)
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
             b[u][v] = ld_d2_stream(basis + (size_t)(t + u) * plane + o + 2 * L * v);
             hh[u][v] = ld_d2(h + (t + u) * ldv + 2 * q + 2 * L * v);
           }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
+        for (int u = 0; u < kUpdTU; ++u)
 #pragma unroll
           for (int v = 0; v < VPL; ++v) {
             s[v].x = fma(b[u][v].x, hh[u][v].x, s[v].x);
