@@ -32,6 +32,7 @@
  *   lanczos.py:152-159  ritz_quadrature (eigh_tridiagonal, tau = y[0,:]^2) -> sdb_ritz_quadrature
  *   lanczos.py:170-177  pool_ritz_quadratures                         -> sdb_pool_nodes
  *   lanczos.py:180-187  blur_nodes (kernels of density.py:58-76)      -> sdb_blur_nodes
+ *   lanczos.py:296-349  cdos_refine (monotone spline CDOS)            -> sdb_cdos_refine
  */
 #ifndef SPECDENS_B200_H
 #define SPECDENS_B200_H
@@ -308,6 +309,18 @@ SDB_API int sdb_pool_nodes(const double* theta, const double* tau2, const int32_
  * density[g] = scale * sum_k w_k K(x_g - theta_k), K Gaussian
  * exp(-x^2/(2 s^2))/sqrt(2 pi s^2) (kind 0) or Lorentzian (s/pi)/(x^2+s^2)
  * (kind 1).  Device pointers. */
+/* cdos_refine (lanczos.py:296-349): theta (sorted ascending) / weights of the
+ * pooled quadrature (count, device); nodes closer than merge_tol are merged at
+ * their weighted mean; a PCHIP spline through (lo, 0), (node_k, cum_k - w_k/2),
+ * (hi, total) is averaged over each grid cell: density[g] = max((cdf(e_{g+1})
+ * - cdf(e_g)) / (e_{g+1} - e_g), 0) with cell edges at grid midpoints (n_pts
+ * == 1: the spline derivative).  Outputs (device): merged nodes/weights
+ * (capacity count), spline_x/y/d (capacity count + 2); n_nodes: HOST out.
+ * Fewer than 2 merged nodes -> SDB_EINVAL.  Synchronises the stream. */
+SDB_API int sdb_cdos_refine(const double* theta, const double* weights, int64_t count, double merge_tol,
+                            double lambda_lb, double lambda_ub, const double* grid, int64_t n_pts,
+                            double* density, double* nodes_out, double* weights_out, double* spline_x,
+                            double* spline_y, double* spline_d, int64_t* n_nodes, void* stream);
 #define SDB_KERNEL_GAUSSIAN 0
 #define SDB_KERNEL_LORENTZIAN 1
 SDB_API int sdb_blur_nodes(const double* theta, const double* w, int64_t count, double scale,

@@ -111,6 +111,7 @@ SIGNATURES = {
     "sdb_ritz_residual_bounds": (_i, [_p, _p, _p, _i64, _i64, _p, _p, _p]),
     "sdb_pool_nodes": (_i, [_p, _p, _p, _i64, _i64, _d, _p, _p, ctypes.POINTER(_i64), _p]),
     "sdb_blur_nodes": (_i, [_p, _p, _i64, _d, _i, _d, _p, _i64, _p, _p]),
+    "sdb_cdos_refine": (_i, [_p, _p, _i64, _d, _d, _d, _p, _i64, _p, _p, _p, _p, _p, _p, ctypes.POINTER(_i64), _p]),
 }
 
 _lock = threading.Lock()

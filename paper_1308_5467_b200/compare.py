@@ -9,9 +9,8 @@ the density once.  The moment-sharing variants ``spectroscopic``,
 the same fused kernels) run through the same kernels.  ``dgl``
 runs its gamma recurrence on the same Legendre moments, and ``haydock``
 evaluates the batched Lanczos tridiagonals' resolvents on the device
-(§8(f)-3).  The remaining reference method (cdos, a monotone-spline
-refinement of the Lanczos staircase) is outside the accelerated path and
-raises ``NotImplementedError``.
+(§8(f)-3); ``cdos`` refines the pooled Ritz staircase with a monotone
+spline on the device (sdb_cdos_refine).
 """
 
 import time
@@ -24,14 +23,14 @@ from . import kpm as K
 from .density import DEFAULT_GRID_POINTS, SpectralDensityEstimate, interval_grid, unit_grid
 from .errors import NumericalFailure
 from .dgl import evaluate_dgl_dos
-from .lanczos import haydock_dos, lanczos_dos
+from .lanczos import cdos_dos, haydock_dos, lanczos_dos
 from .operators import MatvecCounter, apply_spectral_map, as_operator
 
 CHEBYSHEV_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb")
 LEGENDRE_METHODS = ("kpml", "dgl")
 LANCZOS_METHODS = ("lanczos", "haydock", "cdos")
 ALL_METHODS = CHEBYSHEV_METHODS + LEGENDRE_METHODS + LANCZOS_METHODS
-GPU_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb", "kpml", "dgl", "lanczos", "haydock")
+GPU_METHODS = ALL_METHODS
 
 
 def analytic_matvec_count(method, degree, n_vec, product_formula=False):
@@ -118,8 +117,10 @@ def estimate_dos(matrix, interval, method, degree, source, n_vec, sigma=None, et
         grid = interval_grid(interval, grid_points)
         if method == "lanczos":
             est = lanczos_dos(counter, interval, degree, source, n_vec, sigma, grid, threads, device=device)
-        else:
+        elif method == "haydock":
             est = haydock_dos(counter, interval, degree, source, n_vec, eta, grid, threads, device=device)
+        else:
+            est = cdos_dos(counter, interval, degree, source, n_vec, grid, threads, device=device)
     est.params.update({
         "M": degree,
         "n_vec": n_vec,
@@ -153,7 +154,14 @@ from dataclasses import dataclass, field  # noqa: E402
 
 from .density import RegularizationKernel  # noqa: E402
 from .kpm import MomentSequence  # noqa: E402
-from .lanczos import _blur_device, _pool_device, _ritz_device, lanczos_tridiagonals_device  # noqa: E402
+from .lanczos import (  # noqa: E402
+    DEFAULT_MERGE_RTOL,
+    _blur_device,
+    _cdos_device,
+    _pool_device,
+    _ritz_device,
+    lanczos_tridiagonals_device,
+)
 from .metrics import DEFAULT_SUP_CENTERS, check_sup_gaussian_grid, sup_gaussian_device  # noqa: E402
 from .operators import estimate_spectral_interval, resolve  # noqa: E402
 from .reference import blurred_spectrum_device, dense_eigensolve  # noqa: E402
@@ -209,8 +217,7 @@ def run_method_comparison(matrix, methods, degrees, sigma, eta=None, n_vec=100, 
 
     Same arguments, validation order, common random numbers (probe stream =
     repetition), exact-prefix slicing, scoring protocol and rows as the
-    reference.  ``cdos`` (the monotone-spline refinement) is outside the
-    accelerated path and raises ``NotImplementedError``; ``threads`` is ignored.
+    reference; ``threads`` is ignored.
     """
     for m in methods:
         if m not in ALL_METHODS and m != "exact":
@@ -220,8 +227,6 @@ def run_method_comparison(matrix, methods, degrees, sigma, eta=None, n_vec=100, 
     degrees = sorted(set(int(m) for m in degrees))
     if not degrees or degrees[0] < 1:
         raise ValueError("degrees must be positive")
-    if "cdos" in methods:
-        raise NotImplementedError("method 'cdos' is outside the accelerated hot path")
     torch = E._torch()
     device = E.require_cuda(device)
     op = as_operator(matrix)
@@ -241,8 +246,10 @@ def run_method_comparison(matrix, methods, degrees, sigma, eta=None, n_vec=100, 
     need_cheb = any(m in CHEBYSHEV_METHODS for m in methods)
     need_leg = any(m in LEGENDRE_METHODS for m in methods)
     need_lan = any(m in LANCZOS_METHODS for m in methods)
-    if any(m in SPIKE_ESTIMATORS for m in methods):
+    if any(m in SPIKE_ESTIMATORS and m != "cdos" for m in methods):
         check_sup_gaussian_grid(unit_lam, sigma)
+    if "cdos" in methods:
+        check_sup_gaussian_grid(lam_grid, sigma)
 
     errors = {(m, deg): [] for m in methods for deg in degrees}
     masses = {(m, deg): [] for m in methods for deg in degrees}
@@ -271,9 +278,8 @@ def run_method_comparison(matrix, methods, degrees, sigma, eta=None, n_vec=100, 
                       if "dgl" in methods else None)
         exact_lam_h = exact_lam.cpu().numpy()
 
-        def score_spike(est):
-            return sup_gaussian_device(exact_centers, unit_lam_dev, E.to_device(est.density, device), centers_dev,
-                                       sigma, device)
+        def score_spike(density_dev, grid_dev):
+            return sup_gaussian_device(exact_centers, grid_dev, density_dev, centers_dev, sigma, device)
 
         def score_blur(density_dev, ref_dev):
             return torch.max(torch.abs(density_dev - ref_dev))
@@ -286,10 +292,13 @@ def run_method_comparison(matrix, methods, degrees, sigma, eta=None, n_vec=100, 
                     a_p = alpha[:, :dp].contiguous()
                     b_p = beta[:, :dp].contiguous()
                     sd_p = torch.clamp(sd, max=dp).to(torch.int32)
-                    if "lanczos" in methods:
+                    if "lanczos" in methods or "cdos" in methods:
                         th, tw = _ritz_device(a_p[sl], b_p[sl], sd_p[sl], dp, device, stream)
                         nodes, weights = _pool_device(th, tw, sd_p[sl], n_vec, device, stream)
+                    if "lanczos" in methods:
                         lan_dens = _blur_device(nodes, weights, lam_dev, "gaussian", sigma, 1.0, device, stream)
+                    if "cdos" in methods:
+                        cdos_h = _cdos_device(nodes, weights, interval, lam_grid, DEFAULT_MERGE_RTOL, device, stream)[0]
                     if "haydock" in methods:
                         hay_dens = torch.empty_like(lam_dev)
                         _native.call("sdb_haydock", E.ptr(a_p[sl]), E.ptr(b_p[sl]), E.ptr(sd_p[sl]), E.ptr(st[sl]),
@@ -317,10 +326,13 @@ def run_method_comparison(matrix, methods, degrees, sigma, eta=None, n_vec=100, 
                         else:
                             est = evaluate_dgl_dos(moments, interval, sigma, unit_pts, device=device)
                         if method in SPIKE_ESTIMATORS:
-                            err = score_spike(est)
+                            err = score_spike(E.to_device(est.density, device), unit_lam_dev)
                         else:
                             err = score_blur(E.to_device(est.density, device), exact_unit)
                         mass = est.mass()
+                    elif method == "cdos":
+                        err = score_spike(E.to_device(cdos_h, device), lam_dev)
+                        mass = float(np.trapezoid(cdos_h, lam_grid))
                     else:
                         dens = lan_dens if method == "lanczos" else hay_dens
                         err = score_blur(dens, exact_lam)

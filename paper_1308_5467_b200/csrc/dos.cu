@@ -485,6 +485,154 @@ __global__ void blur_kernel(const double* __restrict__ theta, const double* __re
 
 using namespace sdb;
 
+// ---- CDOS: monotone spline through the pooled cumulative staircase -----------------
+// cdos_refine (lanczos.py:296-349).  Stage 1 (one thread: the merge is a
+// running weighted mean, inherently sequential; <= a few 10^4 nodes): merge
+// sorted nodes closer than tol, stair midpoints cumsum - w/2, anchor points
+// (lo, 0) and (hi, total).  Stage 2: PCHIP derivatives (SciPy
+// PchipInterpolator._find_derivatives, same operation order).  Stage 3: the
+// cubic Hermite pieces evaluated at the clipped cell edges as SciPy's PPoly
+// does (power series c3 + c2 s + c1 s^2 + c0 s^3 accumulated in that order,
+// interval by bisection), then density = max(diff(cdf)/diff(edges), 0).
+// Explicit _rn intrinsics: no FMA contraction, like the host evaluation.
+__global__ void cdos_merge_kernel(const double* __restrict__ th, const double* __restrict__ tw, int64_t count,
+                                  double tol, double lb, double ub, double* __restrict__ nodes,
+                                  double* __restrict__ weights, double* __restrict__ xs, double* __restrict__ ys,
+                                  int64_t* __restrict__ kout) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int64_t k = 0;
+  for (int64_t i = 0; i < count; ++i) {
+    const double t = th[i], w = tw[i];
+    if (k > 0 && __dsub_rn(t, nodes[k - 1]) <= tol) {
+      const double total = __dadd_rn(weights[k - 1], w);
+      nodes[k - 1] = __ddiv_rn(__dadd_rn(__dmul_rn(nodes[k - 1], weights[k - 1]), __dmul_rn(t, w)), total);
+      weights[k - 1] = total;
+    } else {
+      nodes[k] = t;
+      weights[k] = w;
+      ++k;
+    }
+  }
+  *kout = k;
+  if (k < 2) return;
+  double cum = 0.0;
+  for (int64_t i = 0; i < k; ++i) {
+    cum = __dadd_rn(cum, weights[i]);
+    xs[i + 1] = nodes[i];
+    ys[i + 1] = __dsub_rn(cum, __dmul_rn(0.5, weights[i]));
+  }
+  const double tiny = 2.2250738585072014e-308;  // np.finfo(float).tiny
+  const double a = __dsub_rn(__dsub_rn(nodes[0], tol), tiny);
+  const double b = __dadd_rn(__dadd_rn(nodes[k - 1], tol), tiny);
+  xs[0] = a < lb ? a : lb;  // min(lambda_lb, ...): the first argument on ties
+  xs[k + 1] = b > ub ? b : ub;
+  ys[0] = 0.0;
+  ys[k + 1] = cum;
+}
+
+__device__ __forceinline__ double sgn_(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
+
+__device__ double pchip_edge(double h0, double h1, double m0, double m1) {
+  double d = __ddiv_rn(__dsub_rn(__dmul_rn(__dadd_rn(__dmul_rn(2.0, h0), h1), m0), __dmul_rn(h0, m1)),
+                       __dadd_rn(h0, h1));
+  const bool mask = sgn_(d) != sgn_(m0);
+  const bool mask2 = (sgn_(m0) != sgn_(m1)) && (fabs(d) > __dmul_rn(3.0, fabs(m0)));
+  if (mask) d = 0.0;
+  else if (mask2) d = __dmul_rn(3.0, m0);
+  return d;
+}
+
+__global__ void cdos_slopes_kernel(const double* __restrict__ xs, const double* __restrict__ ys,
+                                   const int64_t* __restrict__ kin, double* __restrict__ dk) {
+  const int64_t np_ = *kin + 2;  // spline points
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < np_; i += (int64_t)gridDim.x * blockDim.x) {
+    auto h = [&](int64_t j) { return __dsub_rn(xs[j + 1], xs[j]); };
+    auto m = [&](int64_t j) { return __ddiv_rn(__dsub_rn(ys[j + 1], ys[j]), h(j)); };
+    double d;
+    if (i == 0) {
+      d = pchip_edge(h(0), h(1), m(0), m(1));
+    } else if (i == np_ - 1) {
+      d = pchip_edge(h(np_ - 2), h(np_ - 3), m(np_ - 2), m(np_ - 3));
+    } else {
+      const double h0 = h(i - 1), h1 = h(i), m0 = m(i - 1), m1 = m(i);
+      if (sgn_(m1) != sgn_(m0) || m1 == 0.0 || m0 == 0.0) {
+        d = 0.0;
+      } else {
+        const double w1 = __dadd_rn(__dmul_rn(2.0, h1), h0);
+        const double w2 = __dadd_rn(h1, __dmul_rn(2.0, h0));
+        const double whmean = __ddiv_rn(__dadd_rn(__ddiv_rn(w1, m0), __ddiv_rn(w2, m1)), __dadd_rn(w1, w2));
+        d = __ddiv_rn(1.0, whmean);
+      }
+    }
+    dk[i] = d;
+  }
+}
+
+// value (deriv = 0) or first derivative (deriv = 1) of the PCHIP spline at x
+__device__ double pchip_eval(const double* __restrict__ xs, const double* __restrict__ ys,
+                             const double* __restrict__ dk, int64_t np_, double x, int deriv) {
+  int64_t lo = 0, hi = np_ - 1;  // find i with xs[i] <= x < xs[i+1]; x == xs[last] -> last piece
+  if (x >= xs[np_ - 1]) {
+    lo = np_ - 2;
+  } else {
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) / 2;
+      if (x < xs[mid]) hi = mid; else lo = mid;
+    }
+  }
+  const int64_t i = lo;
+  const double dx = __dsub_rn(xs[i + 1], xs[i]);
+  const double slope = __ddiv_rn(__dsub_rn(ys[i + 1], ys[i]), dx);
+  const double t = __ddiv_rn(__dsub_rn(__dadd_rn(dk[i], dk[i + 1]), __dmul_rn(2.0, slope)), dx);
+  const double c0 = __ddiv_rn(t, dx);
+  const double c1 = __dsub_rn(__ddiv_rn(__dsub_rn(slope, dk[i]), dx), t);
+  const double c2 = dk[i], c3 = ys[i];
+  const double sv = __dsub_rn(x, xs[i]);
+  if (deriv == 0) {
+    double res = 0.0, z = 1.0;
+    res = __dadd_rn(res, __dmul_rn(c3, z));
+    z = __dmul_rn(z, sv);
+    res = __dadd_rn(res, __dmul_rn(c2, z));
+    z = __dmul_rn(z, sv);
+    res = __dadd_rn(res, __dmul_rn(c1, z));
+    z = __dmul_rn(z, sv);
+    res = __dadd_rn(res, __dmul_rn(c0, z));
+    return res;
+  }
+  double res = 0.0, z = 1.0;
+  res = __dadd_rn(res, __dmul_rn(__dmul_rn(c2, z), 1.0));
+  z = __dmul_rn(z, sv);
+  res = __dadd_rn(res, __dmul_rn(__dmul_rn(c1, z), 2.0));
+  z = __dmul_rn(z, sv);
+  res = __dadd_rn(res, __dmul_rn(__dmul_rn(c0, z), 3.0));
+  return res;
+}
+
+__global__ void cdos_density_kernel(const double* __restrict__ xs, const double* __restrict__ ys,
+                                    const double* __restrict__ dk, const int64_t* __restrict__ kin,
+                                    const double* __restrict__ grid, int64_t n_pts, double* __restrict__ density) {
+  const int64_t np_ = *kin + 2;
+  if (np_ < 4) return;  // fewer than 2 nodes: reported by the host
+  const double lo = xs[0], hi = xs[np_ - 1];
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < n_pts; g += (int64_t)gridDim.x * blockDim.x) {
+    double v;
+    if (n_pts < 2) {
+      v = pchip_eval(xs, ys, dk, np_, grid[g], 1);
+    } else {
+      // edges (lanczos.py:336-340) of cell g: left and right
+      const double el = g == 0 ? __dsub_rn(grid[0], __dmul_rn(0.5, __dsub_rn(grid[1], grid[0])))
+                               : __dmul_rn(0.5, __dadd_rn(grid[g], grid[g - 1]));
+      const double er = g == n_pts - 1
+                            ? __dadd_rn(grid[n_pts - 1], __dmul_rn(0.5, __dsub_rn(grid[n_pts - 1], grid[n_pts - 2])))
+                            : __dmul_rn(0.5, __dadd_rn(grid[g + 1], grid[g]));
+      const double cl = pchip_eval(xs, ys, dk, np_, fmin(fmax(el, lo), hi), 0);
+      const double cr = pchip_eval(xs, ys, dk, np_, fmin(fmax(er, lo), hi), 0);
+      v = __ddiv_rn(__dsub_rn(cr, cl), __dsub_rn(er, el));
+    }
+    density[g] = v > 0.0 ? v : 0.0;  // np.clip(..., 0.0, None)
+  }
+}
+
 extern "C" {
 
 int sdb_jackson_damping(int64_t degree, double* g, void* stream) {
@@ -665,6 +813,42 @@ int sdb_blur_nodes(const double* theta, const double* w, int64_t count, double s
   int blocks = (int)(n_pts < 65535 ? n_pts : 65535);
   blur_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(theta, w, count, scale, kind, width, grid, n_pts, density);
   SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+
+int sdb_cdos_refine(const double* theta, const double* weights, int64_t count, double merge_tol, double lambda_lb,
+                    double lambda_ub, const double* grid, int64_t n_pts, double* density, double* nodes_out,
+                    double* weights_out, double* spline_x, double* spline_y, double* spline_d, int64_t* n_nodes,
+                    void* stream) {
+  SDB_REQUIRE(theta && weights && nodes_out && weights_out && spline_x && spline_y && spline_d && n_nodes,
+              "NULL argument");
+  SDB_REQUIRE(n_pts == 0 || (grid && density), "NULL argument");
+  SDB_REQUIRE(count >= 0, "bad shape");
+  cudaStream_t s = (cudaStream_t)stream;
+  int64_t* dk = nullptr;
+  SDB_CUDA(cudaMallocAsync(&dk, sizeof(int64_t), s));
+  SDB_CUDA(cudaMemsetAsync(dk, 0, sizeof(int64_t), s));
+  if (count > 0) {
+    cdos_merge_kernel<<<1, 32, 0, s>>>(theta, weights, count, merge_tol, lambda_lb, lambda_ub, nodes_out, weights_out,
+                                      spline_x, spline_y, dk);
+    SDB_CHECK_LAUNCH();
+  }
+  SDB_CUDA(cudaMemcpyAsync(n_nodes, dk, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SDB_CUDA(cudaStreamSynchronize(s));
+  if (*n_nodes < 2) {
+    cudaFreeAsync(dk, s);
+    return fail(SDB_EINVAL, "need at least 2 distinct Ritz nodes for the spline");
+  }
+  const int64_t np_ = *n_nodes + 2;
+  cdos_slopes_kernel<<<(unsigned)((np_ + 255) / 256), 256, 0, s>>>(spline_x, spline_y, dk, spline_d);
+  SDB_CHECK_LAUNCH();
+  if (n_pts > 0) {
+    cdos_density_kernel<<<(unsigned)((n_pts + 255) / 256), 256, 0, s>>>(spline_x, spline_y, spline_d, dk, grid, n_pts,
+                                                                        density);
+    SDB_CHECK_LAUNCH();
+  }
+  SDB_CUDA(cudaFreeAsync(dk, s));
   return SDB_OK;
 }
 

@@ -15,7 +15,8 @@ import numpy as np
 
 from . import _native
 from . import engine as E
-from .compare import GPU_METHODS
+# methods with a sharded implementation here (one all-gather of per-probe rows)
+SHARDED_METHODS = ("kpm", "kpm-jackson", "lanczos")
 from .density import DEFAULT_GRID_POINTS, SpectralDensityEstimate, interval_grid, unit_grid
 from .errors import NumericalFailure
 from .operators import MatvecCounter, apply_spectral_map, as_operator
@@ -84,8 +85,8 @@ def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=
 
     from .lanczos import _pool_device, _blur_device, lanczos_quadrature_device
 
-    if method not in GPU_METHODS:
-        raise ValueError(f"sharded estimates support {GPU_METHODS}")
+    if method not in SHARDED_METHODS:
+        raise ValueError(f"sharded estimates support {SHARDED_METHODS}")
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     start, count = shard_range(n_vec, world, rank)

@@ -434,3 +434,95 @@ def haydock_dos(op, interval, steps, source, n_vec, eta=None, grid=None, threads
         grid, density, interval, method="haydock",
         params={"M": steps, "n_vec": n_vec, "eta": eta, "truncation_indicator": float(packed[-1])},
     )
+
+
+# ---------------------------------------------------------------------------
+# CDOS (lanczos.py:296-368): a monotone PCHIP spline through the pooled
+# cumulative staircase, averaged over each grid cell -- one merge pass, the
+# PCHIP slopes and the cell averages on the device (sdb_cdos_refine).
+
+DEFAULT_MERGE_RTOL = 1e-10
+
+
+class PchipCdf:
+    """The CDF spline of a CDOS estimate: breakpoints, values and PCHIP slopes
+    (what SciPy's PchipInterpolator holds).  Calling it evaluates the cubic
+    Hermite pieces on the host -- an inspection helper, not the estimator."""
+
+    def __init__(self, x, y, d):
+        self.x, self.y, self.d = np.asarray(x), np.asarray(y), np.asarray(d)
+
+    def __call__(self, xq):
+        xq = np.asarray(xq, dtype=float)
+        i = np.clip(np.searchsorted(self.x, xq, side="right") - 1, 0, len(self.x) - 2)
+        h = self.x[i + 1] - self.x[i]
+        s = xq - self.x[i]
+        m = (self.y[i + 1] - self.y[i]) / h
+        t = (self.d[i] + self.d[i + 1] - 2 * m) / h
+        return self.y[i] + self.d[i] * s + ((m - self.d[i]) / h - t) * s**2 + t / h * s**3
+
+
+def _cdos_device(theta_dev, weights_dev, interval, grid, merge_rtol, device, stream):
+    torch = E._torch()
+    count = theta_dev.numel()
+    nodes = torch.empty(max(count, 1), dtype=torch.float64, device=device)
+    wts = torch.empty_like(nodes)
+    sx = torch.empty(count + 2, dtype=torch.float64, device=device)
+    sy = torch.empty_like(sx)
+    sd = torch.empty_like(sx)
+    g = E.to_device(grid, device)
+    dens = torch.empty_like(g)
+    k = ctypes.c_int64(0)
+    _native.call("sdb_cdos_refine", E.ptr(theta_dev) if count else None, E.ptr(weights_dev) if count else None,
+                 count, float(merge_rtol * interval.width), float(interval.lambda_lb), float(interval.lambda_ub),
+                 E.ptr(g), g.numel(), E.ptr(dens), E.ptr(nodes), E.ptr(wts), E.ptr(sx), E.ptr(sy), E.ptr(sd),
+                 ctypes.byref(k), stream)
+    kk = k.value
+    packed = torch.cat([dens, nodes[:kk], wts[:kk], sx[:kk + 2], sy[:kk + 2], sd[:kk + 2]]).cpu().numpy()
+    n = g.numel()
+    parts = np.split(packed, np.cumsum([n, kk, kk, kk + 2, kk + 2]))
+    return parts[0], parts[1], parts[2], PchipCdf(parts[3], parts[4], parts[5])
+
+
+def cdos_refine(quad, interval, grid=None, merge_rtol=DEFAULT_MERGE_RTOL, device=None):
+    """Differentiate a monotone spline through the cumulative staircase (lanczos.py:296-349)."""
+    if grid is None:
+        grid = interval_grid(interval, DEFAULT_GRID_POINTS)
+    grid = np.asarray(grid, dtype=float)
+    torch = E._torch()
+    device = E.require_cuda(device)
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        th = E.to_device(np.asarray(quad.theta, dtype=float).ravel(), device)
+        tw = E.to_device(np.asarray(quad.tau_sq, dtype=float).ravel(), device)
+        order = torch.argsort(th, stable=True)
+        density, nodes, weights, cdf = _cdos_device(th[order].contiguous(), tw[order].contiguous(), interval, grid,
+                                                    merge_rtol, device, stream)
+    return SpectralDensityEstimate.from_original(
+        grid, density, interval, method="cdos", params={"cdf": cdf, "nodes": nodes, "node_weights": weights},
+    )
+
+
+def cdos_dos(op, interval, steps, source, n_vec, grid=None, threads=None, reorth="full", device=None):
+    """Pool per-probe Ritz quadratures and refine the cumulative staircase (lanczos.py:352-368)."""
+    _check_args(reorth, steps, resolve(op).dim)
+    if grid is None:
+        grid = interval_grid(interval, DEFAULT_GRID_POINTS)
+    grid = np.asarray(grid, dtype=float)
+    torch = E._torch()
+    device = E.require_cuda(device)
+    res, theta, tau2, sd, _ = lanczos_quadrature_device(op, steps, source, n_vec, reorth=reorth, device=device)
+    with torch.cuda.device(device):
+        stream = E.stream_ptr(device)
+        nodes_p, weights_p = _pool_device(theta, tau2, sd, n_vec, device, stream)  # sorted by theta
+        density, nodes, weights, cdf = _cdos_device(nodes_p, weights_p, interval, grid, DEFAULT_MERGE_RTOL, device,
+                                                    stream)
+        ritz_nodes = nodes_p.cpu().numpy()
+        ritz_weights = weights_p.cpu().numpy()
+    for c in res.counters:
+        c.count += int(sd.sum().item())
+    est = SpectralDensityEstimate.from_original(
+        grid, density, interval, method="cdos", params={"cdf": cdf, "nodes": nodes, "node_weights": weights},
+    )
+    est.params.update({"M": steps, "n_vec": n_vec, "ritz_nodes": ritz_nodes, "ritz_weights": ritz_weights})
+    return est

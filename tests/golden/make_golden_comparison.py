@@ -23,14 +23,14 @@ from specdens import (  # noqa: E402
     run_method_comparison,
 )
 
-METHODS = ["kpm", "kpm-jackson", "spectroscopic", "delta-cheb", "kpml", "dgl", "lanczos", "haydock", "exact"]
+METHODS = ["kpm", "kpm-jackson", "spectroscopic", "delta-cheb", "kpml", "dgl", "lanczos", "haydock", "cdos", "exact"]
 
 CASES = {
     # the reference's own conftest matrix (50-dim, default bumps), interval and spectrum passed in
     "small_lap": dict(nx=10, ny=5, methods=METHODS, degrees=[16, 8, 30, 8], sigma=0.5, eta=None, n_vec=8, reps=3,
                       seed=0, probe_kind="gaussian", grid_points=512, pass_interval=True),
     # 24-dim: Lanczos steps capped at the dimension; interval and spectrum computed inside
-    "tiny_capped": dict(nx=6, ny=4, methods=["kpm", "lanczos", "haydock", "dgl", "exact"], degrees=[10, 30],
+    "tiny_capped": dict(nx=6, ny=4, methods=["kpm", "lanczos", "haydock", "cdos", "dgl", "exact"], degrees=[10, 30],
                         sigma=0.6, eta=0.3, n_vec=5, reps=4, seed=3, probe_kind="rademacher", grid_points=600,
                         pass_interval=False),
 }
