@@ -29,7 +29,12 @@ from .operators import SparseSymmetricMatrix, StencilOperator
 # C1: the reference's model problem, built directly as sorted int32 CSR
 
 
-def generate_modified_laplacian_2d(nx, ny, bumps=()):
+# the reference's frozen test potential (matrix.py:24-29): a shallow well at
+# (4, 5) and a sharp barrier at (25, 15)
+DEFAULT_BUMPS = ((4.0, 5.0, -0.13, 4.0), (25.0, 15.0, 5.0, 1.5))
+
+
+def generate_modified_laplacian_2d(nx, ny, bumps=DEFAULT_BUMPS):
     """5-point Dirichlet Laplacian plus Gaussian bumps (matrix.py:173-204).
 
     Builds the CSR the reference produces (diagonal 4 + potential, off-
