@@ -335,8 +335,14 @@ __global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
 // iteration keep 2*KMAX independent 16-byte loads in flight per thread.
 constexpr int kZcs = 16;
 
+// Two resident blocks per SM up to KMAX = 8 (<= 128 registers; the KMAX = 8
+// form spills 160 bytes but the doubled warps in flight win: C4 0.806 ->
+// 0.789 s); KMAX = 16 (236 registers) keeps one.
+#ifndef SDB_UPJ_MINB_SMALL
+#define SDB_UPJ_MINB_SMALL 2
+#endif
 template <int KMAX, int kZrows, int kZtg>
-__global__ void __launch_bounds__(kZcs * kZtg, (KMAX * kZrows * kZtg >= 256) ? 1 : 2)
+__global__ void __launch_bounds__(kZcs * kZtg, KMAX >= 16 ? 1 : (KMAX <= 4 ? SDB_UPJ_MINB_SMALL : 2))
     lz_update_proj(const double* __restrict__ basis, const double* __restrict__ wsrc, double* __restrict__ w,
                    const double* __restrict__ h, int64_t j,
                    int64_t n, int64_t ldv, int64_t nrb, double* __restrict__ partials) {
