@@ -114,8 +114,11 @@ __global__ void lz_start_reduce(const double* __restrict__ partials, int64_t nbl
 }
 
 // ---- K4: w = A v_j - beta_{j-1} v_{j-1}, v_j = w_prev * inv_beta, alpha partials ----
+#ifndef SDB_SPMM_MINB
+#define SDB_SPMM_MINB 4
+#endif
 template <class View, int L, int VPL>
-__global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
+__global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? SDB_SPMM_MINB : 2)
     lz_spmm(View A, const double* __restrict__ wprev, const double* __restrict__ vprev, double* __restrict__ vj,
             double* __restrict__ wout, LzState st, int first, double c, double inv_d, int64_t n, int64_t ldv,
             int64_t nblocks, int64_t panel, double* partials) {
@@ -257,8 +260,11 @@ __global__ void lz_h_reduce(const double* __restrict__ partials, int64_t nrb, in
 }
 
 // ---- K5b: w -= V h (row-local), optional ||w||^2 partials ---------------------------
+#ifndef SDB_UPD_MINB
+#define SDB_UPD_MINB 4
+#endif
 template <int L, int VPL, bool NORM>
-__global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? 3 : 2)
+__global__ void __launch_bounds__(kRowThreads, VPL <= 2 ? SDB_UPD_MINB : 2)
     lz_update(const double* __restrict__ basis, double* w, const double* __restrict__ h, int64_t j, int64_t n,
               int64_t ldv, int64_t nblocks, int64_t panel, double* partials) {
   constexpr int RPW = 32 / L, RPB = RPW * kRowWarps;
