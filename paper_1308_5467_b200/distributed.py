@@ -15,11 +15,13 @@ import numpy as np
 
 from . import _native
 from . import engine as E
-# methods with a sharded implementation here (one all-gather of per-probe rows)
-SHARDED_METHODS = ("kpm", "kpm-jackson", "lanczos")
 from .density import DEFAULT_GRID_POINTS, SpectralDensityEstimate, interval_grid, unit_grid
 from .errors import NumericalFailure
 from .operators import MatvecCounter, apply_spectral_map, as_operator
+
+# every estimate_dos method: Chebyshev / Legendre families gather per-probe
+# moment rows, the Lanczos family gathers per-probe Ritz or tridiagonal rows
+SHARDED_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb", "kpml", "dgl", "lanczos", "haydock", "cdos")
 
 
 def shard_range(n_vec, world, rank):
@@ -75,8 +77,8 @@ class _ShiftedSource:
 
 
 def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=None, grid_points=DEFAULT_GRID_POINTS,
-                         product_formula=False, group=None):
-    """``estimate_dos`` with the probes sharded over the ranks of ``group``.
+                         product_formula=False, group=None, eta=None):
+    """``estimate_dos`` with the probes sharded over the ranks of ``group`` (any method).
 
     Must be called collectively; every rank returns the same estimate.
     """
@@ -95,6 +97,10 @@ def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=
     dev = torch.cuda.current_device()
     shifted = _ShiftedSource(source, start)
     counter = MatvecCounter(as_operator(matrix))
+    if product_formula and method not in ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb"):
+        raise ValueError("the product formula only applies to Chebyshev moments")
+    if method in ("dgl", "lanczos") and (sigma is None or not sigma > 0):
+        raise ValueError(f"method {method} requires a positive sigma")
     if method in ("kpm", "kpm-jackson"):
         mode = _native.SDB_CHEB_DOUBLING if product_formula else _native.SDB_CHEB_DIRECT
         run = E.run_chebyshev(apply_spectral_map(counter, interval), degree, shifted, count, mode, device=dev)
@@ -114,9 +120,59 @@ def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=
                                                  method=method, params={"degree": degree, "moments": packed[:m1]})
         if method == "kpm-jackson":
             est.params["damping"] = "jackson"
+    elif method in ("spectroscopic", "delta-cheb", "kpml", "dgl"):
+        from . import kpm as K
+        from .dgl import evaluate_dgl_dos
+
+        legendre = method in ("kpml", "dgl")
+        mode = (_native.SDB_LEGENDRE if legendre else
+                (_native.SDB_CHEB_DOUBLING if product_formula else _native.SDB_CHEB_DIRECT))
+        run = E.run_chebyshev(apply_spectral_map(counter, interval), degree, shifted, count, mode, device=dev)
+        zeta_pp = gather_probe_rows(run.zeta_pp, n_vec, group)
+        zeta_dev, flag = E.mean_moments(zeta_pp, dev)
+        packed = torch.cat([zeta_dev, flag.to(torch.float64)]).cpu().numpy()
+        if packed[-1] != 0.0 or not np.all(np.isfinite(packed[:-1])):
+            raise NumericalFailure(E.SPECTRUM_ESCAPE_HINT)
+        counter.count += n_vec * run.matvecs_per_probe
+        moments = K.MomentSequence(zeta=packed[:-1], degree=degree, n_vec=n_vec,
+                                   basis="legendre" if legendre else "chebyshev", n=run.n)
+        grid = unit_grid(grid_points)
+        if method == "spectroscopic":
+            est = K.spectroscopic_dos(moments, interval, grid, device=dev)
+        elif method == "delta-cheb":
+            est = K.delta_chebyshev_dos(moments, interval, grid, device=dev)
+        elif method == "kpml":
+            est = K.evaluate_kpml_dos(moments, interval, grid, device=dev)
+        else:
+            est = evaluate_dgl_dos(moments, interval, sigma, grid, device=dev)
+    elif method == "haydock":
+        from .lanczos import lanczos_tridiagonals_device
+
+        grid = interval_grid(interval, grid_points)
+        if eta is None:
+            eta = interval.width / (2.0 * len(grid))
+        if not eta > 0:
+            raise ValueError("eta must be positive")
+        _, alpha, beta, sd, st = lanczos_tridiagonals_device(counter, degree, shifted, count, device=dev)
+        a_all = gather_probe_rows(alpha, n_vec, group).contiguous()
+        b_all = gather_probe_rows(beta, n_vec, group).contiguous()
+        sds = gather_probe_rows(sd.view(-1, 1).to(torch.float64), n_vec, group).view(-1).to(torch.int32)
+        sts = gather_probe_rows(st.view(-1, 1).to(torch.float64), n_vec, group).view(-1).to(torch.int32)
+        stream = E.stream_ptr(dev)
+        g = E.to_device(grid, dev)
+        dens = torch.empty_like(g)
+        tpts = torch.empty_like(g)
+        trunc = torch.empty(1, dtype=torch.float64, device=dev)
+        _native.call("sdb_haydock", E.ptr(a_all), E.ptr(b_all), E.ptr(sds), E.ptr(sts), n_vec, degree, E.ptr(g),
+                     g.numel(), float(eta), E.ptr(dens), E.ptr(tpts), E.ptr(trunc), stream)
+        packed = torch.cat([dens, trunc]).cpu().numpy()
+        counter.count = int(sds.sum().item())
+        est = SpectralDensityEstimate.from_original(
+            grid, packed[:-1], interval, method="haydock",
+            params={"M": degree, "n_vec": n_vec, "eta": eta, "truncation_indicator": float(packed[-1])})
     else:
-        if sigma is None or not sigma > 0:
-            raise ValueError("method lanczos requires a positive sigma")
+        from .lanczos import DEFAULT_MERGE_RTOL, _cdos_device
+
         grid = interval_grid(interval, grid_points)
         _, theta, tau2, sd, _ = lanczos_quadrature_device(counter, degree, shifted, count, device=dev)
         th = gather_probe_rows(theta, n_vec, group)
@@ -124,13 +180,21 @@ def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=
         sds = gather_probe_rows(sd.view(-1, 1).to(torch.float64), n_vec, group).view(-1).to(torch.int32)
         stream = E.stream_ptr(dev)
         nodes, weights = _pool_device(th, tw, sds, n_vec, dev, stream)
-        dens = _blur_device(nodes, weights, E.to_device(grid, dev), "gaussian", sigma, 1.0, dev, stream)
-        density = dens.cpu().numpy()
         counter.count = int(sds.sum().item())
-        est = SpectralDensityEstimate.from_parts(grid, density, grid, density, interval, method="lanczos",
-                                                 params={"M": degree, "n_vec": n_vec, "sigma": sigma,
-                                                         "ritz_nodes": nodes.cpu().numpy(),
-                                                         "ritz_weights": weights.cpu().numpy()})
+        if method == "lanczos":
+            dens = _blur_device(nodes, weights, E.to_device(grid, dev), "gaussian", sigma, 1.0, dev, stream)
+            density = dens.cpu().numpy()
+            est = SpectralDensityEstimate.from_parts(grid, density, grid, density, interval, method="lanczos",
+                                                     params={"M": degree, "n_vec": n_vec, "sigma": sigma,
+                                                             "ritz_nodes": nodes.cpu().numpy(),
+                                                             "ritz_weights": weights.cpu().numpy()})
+        else:
+            density, mnodes, mweights, cdf = _cdos_device(nodes, weights, interval, grid, DEFAULT_MERGE_RTOL, dev,
+                                                          stream)
+            est = SpectralDensityEstimate.from_original(
+                grid, density, interval, method="cdos",
+                params={"cdf": cdf, "nodes": mnodes, "node_weights": mweights, "ritz_nodes": nodes.cpu().numpy(),
+                        "ritz_weights": weights.cpu().numpy()})
     est.params.update({"M": degree, "n_vec": n_vec, "matvec_count": counter.count, "world_size": world})
     if product_formula:
         est.params["product_formula"] = True

@@ -34,13 +34,15 @@ def nccl_group():
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("method", ["kpm-jackson", "lanczos"])
+@pytest.mark.parametrize("method", ["kpm-jackson", "kpm", "spectroscopic", "delta-cheb", "kpml", "dgl", "lanczos",
+                                    "haydock", "cdos"])
 def test_sharded_estimate_matches_single(nccl_group, method):
     op = W.anderson_3d(10)
     iv = W.gershgorin_interval(op)
     src = sdb.ProbeVectorSource("gaussian", seed=3, dim=op.dim)
-    kw = {"sigma": 0.05} if method == "lanczos" else {"product_formula": True}
-    deg = 30 if method == "lanczos" else 61
+    kw = {"kpm-jackson": {"product_formula": True}, "spectroscopic": {"product_formula": True},
+          "lanczos": {"sigma": 0.05}, "dgl": {"sigma": 0.2}, "haydock": {"eta": 0.1}}.get(method, {})
+    deg = 30 if method in ("lanczos", "haydock", "cdos") else 61
     one = sdb.estimate_dos(op, iv, method, deg, src, 7, grid_points=300, **kw)
     sh = D.estimate_dos_sharded(op, iv, method, deg, src, 7, grid_points=300, **kw)
     np.testing.assert_allclose(sh.density, one.density, rtol=0, atol=1e-13)
