@@ -8,6 +8,13 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+# In the build container the reference package is importable from its source
+# tree; the CPU-only cross-checks against it (tests/test_host_logic.py) then
+# run instead of skipping.  It is appended (never shadows this repo) and is
+# absent on the GPU box, where nothing reads it.
+_REF_SRC = "/root/reference/pkg/src"
+if os.path.isdir(_REF_SRC) and _REF_SRC not in sys.path:
+    sys.path.append(_REF_SRC)
 
 
 def pytest_configure(config):
