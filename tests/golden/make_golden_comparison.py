@@ -33,6 +33,10 @@ CASES = {
     "tiny_capped": dict(nx=6, ny=4, methods=["kpm", "lanczos", "haydock", "cdos", "dgl", "exact"], degrees=[10, 30],
                         sigma=0.6, eta=0.3, n_vec=5, reps=4, seed=3, probe_kind="rademacher", grid_points=600,
                         pass_interval=False),
+    # exhaustive basis probes (sqrt(n) e_l) on a 12-dim matrix: exact traces, Lanczos to full depth
+    "basis_full": dict(nx=4, ny=3, methods=["kpm", "kpm-jackson", "lanczos", "cdos", "exact"], degrees=[5, 12],
+                       sigma=0.8, eta=None, n_vec=12, reps=2, seed=0, probe_kind="basis", grid_points=400,
+                       pass_interval=False),
 }
 
 

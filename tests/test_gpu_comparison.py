@@ -36,7 +36,7 @@ def _case(z, name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["small_lap", "tiny_capped"])
+@pytest.mark.parametrize("name", ["small_lap", "tiny_capped", "basis_full"])
 def test_comparison_matches_reference_rows(name):
     z = np.load(GOLDEN)
     mat, methods, degrees, sigma, kwargs = _case(z, name)

@@ -201,7 +201,7 @@ def test_comparison_golden_rows_are_consistent():
     import os
 
     z = np.load(os.path.join(os.path.dirname(__file__), "golden", "method_comparison.npz"))
-    for name in ("small_lap", "tiny_capped"):
+    for name in ("small_lap", "tiny_capped", "basis_full"):
         p = name + "/"
         methods = [str(m) for m in z[p + "row_method"]]
         errs = z[p + "row_errors"]
