@@ -130,6 +130,13 @@ SDB_API int sdb_matrix_create_csr(int device, int64_t n, int64_t nnz, const int6
 SDB_API int sdb_matrix_create_stencil(int device, const sdb_stencil_desc* desc, const double* diag,
                               void* stream, sdb_matrix** out);
 SDB_API int sdb_matrix_get_info(const sdb_matrix* m, sdb_matrix_info* info);
+/* Band + far split of a CSR handle (done at upload when the matrix has a dense
+ * symmetric band, e.g. BASELINE config 3; matrix.py:35-109 storage, read by
+ * the probe-sliced step kernel): half_width = 0 when the matrix is not split;
+ * far_entries = stored off-band entries (pair-padded); bytes_per_pass = bytes
+ * one probe slice streams (band diagonals + far pairs + row pointers). */
+SDB_API int sdb_matrix_band_info(const sdb_matrix* m, int32_t* half_width, int64_t* far_entries,
+                                 int64_t* bytes_per_pass);
 SDB_API void sdb_matrix_destroy(sdb_matrix* m);
 
 /* Deterministic device-side pack: probes_t is n_vec x n (probe-major, device),

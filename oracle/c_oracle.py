@@ -21,6 +21,8 @@ def _load():
         lib.oracle_cheb_moments.argtypes = [i64, p, p, p, d, d, i64, i, i64, p, p, i]
         lib.oracle_cheb_moments.restype = i
         lib.oracle_max_threads.restype = i
+        lib.oracle_stencil_moments.argtypes = [i64, i64, i64, i, p, p, p, d, d, i64, i, i64, p, p, i]
+        lib.oracle_stencil_moments.restype = i
         _lib = lib
     return _lib
 
@@ -43,4 +45,22 @@ def cheb_moments(csr, c, d, degree, probes, mode="doubling", threads=0):
                                  out.ctypes.data, int(threads))
     if rc:
         raise RuntimeError(f"oracle_cheb_moments failed ({rc})")
+    return out
+
+
+def stencil_moments(op, c, d, degree, probes, mode="doubling", threads=0):
+    """Per-probe moments of a periodic StencilOperator (no CSR is built)."""
+    lib = _load()
+    nx, ny, nz = op.shape
+    offs = np.ascontiguousarray(np.asarray(op.offsets, dtype=np.int32).reshape(-1, 3))
+    w = np.ascontiguousarray(op.weights, dtype=np.float64)
+    diag = np.ascontiguousarray(op.diag, dtype=np.float64)
+    probes = np.ascontiguousarray(probes, dtype=np.float64)
+    n_vec, n = probes.shape
+    out = np.empty((n_vec, degree + 1))
+    rc = lib.oracle_stencil_moments(nx, ny, nz, len(w), offs.ctypes.data, w.ctypes.data, diag.ctypes.data, float(c),
+                                    float(d), int(degree), 0 if mode == "direct" else 1, n_vec, probes.ctypes.data,
+                                    out.ctypes.data, int(threads))
+    if rc:
+        raise RuntimeError(f"oracle_stencil_moments failed ({rc})")
     return out

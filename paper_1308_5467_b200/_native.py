@@ -75,6 +75,7 @@ SIGNATURES = {
     "sdb_matrix_create_csr": (_i, [_i, _i64, _i64, _p, _p, _i, _p, _p, ctypes.POINTER(_p)]),
     "sdb_matrix_create_stencil": (_i, [_i, ctypes.POINTER(SdbStencilDesc), _p, _p, ctypes.POINTER(_p)]),
     "sdb_matrix_get_info": (_i, [_p, ctypes.POINTER(SdbMatrixInfo)]),
+    "sdb_matrix_band_info": (_i, [_p, ctypes.POINTER(_i32), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "sdb_matrix_destroy": (None, [_p]),
     "sdb_pack_probes": (_i, [_p, _i64, _i64, _i64, _p, _p]),
     "sdb_unpack_block": (_i, [_p, _i64, _i64, _i64, _p, _p]),

@@ -747,8 +747,8 @@ static int launch_plan_step(const sdb_matrix* m, const StepPlan& P, int64_t degr
 }
 
 static int launch_reduce(const StepPlan& P, int64_t n_vec, int64_t degree, int mode, const double* partials,
-                         double* zeta_pp, cudaStream_t s) {
-  const int64_t nb = P.a.nblocks, ldv = P.g.ldv, slots = degree + 1;
+                         double* zeta_pp, cudaStream_t s, int64_t ldv_override = 0) {
+  const int64_t nb = P.a.nblocks, ldv = ldv_override > 0 ? ldv_override : P.g.ldv, slots = degree + 1;
   const int64_t nch = (nb + kReduceChunk - 1) / kReduceChunk;
   // stage buffer sits behind the largest possible partials array (cheb_layout)
   const int64_t bmax = 8LL * num_sms(P.device);
@@ -763,6 +763,62 @@ static int launch_reduce(const StepPlan& P, int64_t n_vec, int64_t degree, int m
   if (b2 > 65535) b2 = 65535;
   cheb_reduce_stage2<<<b2, 256, 0, s>>>(stage, nch, ldv, n_vec, degree, mode, zeta_pp);
   SDB_CHECK_LAUNCH();
+  return SDB_OK;
+}
+
+// Moment run on the probe-sliced band + far path (band.cu): slice-major copy
+// of the probes, PDL-chained step launches, K2 over the band kernel's partial
+// rows.  Timed from the probe copy, like the z-march padding.
+static int band_moments(const sdb_matrix* m, const StepPlan& P0, const BandPlan& bp, int64_t n_vec, int64_t degree,
+                        int mode, const double* probes, double* zeta_pp, void* workspace, cudaStream_t s,
+                        float* step_ms) {
+  double* v0b = (double*)workspace;
+  double* bufA = (double*)((char*)workspace + bp.block_bytes);
+  double* bufB = (double*)((char*)workspace + 2 * bp.block_bytes);
+  double* partials = (double*)((char*)workspace + 3 * bp.block_bytes);
+  const int64_t steps = (mode == SDB_CHEB_DOUBLING) ? (degree + 1) / 2 : degree;
+  PdlScope pdl_scope;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (step_ms) {
+    SDB_CUDA(cudaEventCreate(&e0));
+    SDB_CUDA(cudaEventCreate(&e1));
+    SDB_CUDA(cudaEventRecord(e0, s));
+  }
+  int rc = band_pack(m, bp, probes, P0.g.ldv, v0b, bufA, bufB, s);
+  if (rc) return rc;
+  const double* cur = v0b;
+  const double* prev = nullptr;
+  for (int64_t k = 0; k < steps; ++k) {
+    double* next = k == 0 ? bufA : (k == 1 ? bufB : const_cast<double*>(prev));
+    StepArgs a = P0.a;
+    a.partials = partials;
+    a.v0 = v0b;
+    a.x = cur;
+    a.prev = prev;
+    a.next = next;
+    a.slot0 = (k == 0) ? 0 : -1;
+    set_step_scalars(a, k);
+    if (mode == SDB_CHEB_DOUBLING) {
+      a.slotB = (2 * k + 1 <= degree) ? (int)(2 * k + 1) : -1;
+      a.slotA = (2 * k + 2 <= degree) ? (int)(2 * k + 2) : -1;
+    } else {
+      a.slotA = (int)(k + 1);
+      a.slotB = -1;
+    }
+    if ((rc = band_launch_step(m, bp, a, k == 0, mode, s))) return rc;
+    prev = cur;
+    cur = next;
+  }
+  if (step_ms) SDB_CUDA(cudaEventRecord(e1, s));
+  StepPlan P = P0;
+  P.a.nblocks = bp.grid;
+  if ((rc = launch_reduce(P, n_vec, degree, mode, partials, zeta_pp, s, bp.ldvb))) return rc;
+  if (step_ms) {
+    SDB_CUDA(cudaEventSynchronize(e1));
+    SDB_CUDA(cudaEventElapsedTime(step_ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
   return SDB_OK;
 }
 
@@ -781,9 +837,17 @@ int sdb_cheb_workspace_size(const sdb_matrix* m, int64_t n_vec, int64_t degree, 
   SDB_REQUIRE(mode == SDB_CHEB_DIRECT || mode == SDB_CHEB_DOUBLING, "unknown moment mode %d", mode);
   Geometry g = choose_geometry(n_vec);
   size_t bb, pb;
+  BandPlan bp;
+  int rc = band_plan(m, n_vec, mode, &bp);
+  if (rc) return rc;
+  if (bp.on) {  // slice-major probe copy + two recurrence blocks + partials
+    cheb_layout(m, bp.ldvb, degree, &bb, &pb);
+    *bytes = 3 * bp.block_bytes + pb;
+    return SDB_OK;
+  }
   cheb_layout(m, g.ldv, degree, &bb, &pb);
   ZmPlan zp;
-  int rc = zm_plan(m, g.ldv, mode, &zp);
+  rc = zm_plan(m, g.ldv, mode, &zp);
   if (rc) return rc;
   // z-march path: padded probe copy + two padded recurrence buffers (fused
   // pairs: + a third and the padded diagonal)
@@ -796,6 +860,8 @@ const char* sdb_cheb_kernel(const sdb_matrix* m, int64_t n_vec, int mode) {
   mode = split_mode(mode, &leg_);
   if (!m || n_vec < 1 || n_vec > SDB_MAX_BATCH) return "";
   const Geometry g = choose_geometry(n_vec);
+  BandPlan bp;
+  if (band_plan(m, n_vec, mode, &bp) == SDB_OK && bp.on) return "cheb_step_band";
   ZmPlan zp;
   if (zm_plan(m, g.ldv, mode, &zp) == SDB_OK && zp.on) return zp.name;
   if (m->format == SDB_FMT_CSR) return "cheb_step_csr";
@@ -822,6 +888,14 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
   StepPlan P;
   if ((rc = plan_steps(m, n_vec, mode, c, d, &P))) return rc;
   P.a.legendre = legendre;
+  {
+    const int64_t steps_b = (mode == SDB_CHEB_DOUBLING) ? (degree + 1) / 2 : degree;
+    BandPlan bp;
+    if ((rc = band_plan(m, n_vec, mode, &bp))) return rc;
+    if (bp.on && steps_b > 0)
+      return band_moments(m, P, bp, n_vec, degree, mode, probes, zeta_pp, workspace, (cudaStream_t)stream,
+                          step_ms);
+  }
   size_t bb, pb;
   cheb_layout(m, P.g.ldv, degree, &bb, &pb);
   ZmPlan zp;

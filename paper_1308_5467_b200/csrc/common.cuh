@@ -48,6 +48,16 @@ struct DeviceGuard {
 
 int num_sms(int device);
 
+// Band + far split of a freshly uploaded CSR matrix (band.cu).  Leaves the
+// matrix unsplit (hb = 0) when it has no dense symmetric band; returns an
+// error code only on CUDA failures.
+}  // namespace sdb
+struct sdb_matrix;
+namespace sdb {
+int band_build(sdb_matrix* m, cudaStream_t s);
+// zero guard rows/diagonal entries before and after the band data
+__host__ __device__ constexpr int band_pad(int hb) { return (hb + 7) & ~7; }
+
 // ---- matrix handle ---------------------------------------------------------
 struct StencilDev {
   int64_t nx, ny, nz;
@@ -76,6 +86,20 @@ struct sdb_matrix {
   int nterms = 0, center_pos = 0, mx = 0, my = 0, mz = 0;
   int shape = 0;              // SDB_SHAPE_*: specialised grid kernel available
   int zghost = 0;             // z-slab of a row partition (no z wrap, ghost planes)
+  // band + far split of a CSR matrix (band.cu): the dense band |i-j| <= hb as
+  // symmetric upper diagonals, the rest (far entries) in SELL-8 slots
+  int hb = 0;                 // 0: no split
+  int64_t ustride = 0;        // doubles per diagonal of bu
+  double* bu = nullptr;       // [hb+1][ustride]: bu[d*ustride + kBandPad(hb) + i] = A[i][i+d]
+  // far entries, SELL-8: chunk c = rows 8c..8c+7 holds slots [fptr[c], fmid[c])
+  // (lower segments) and [fmid[c], fptr[c+1]) (upper segments); slot s stores
+  // one entry per row of the chunk at fcol/fval[8s + r] (column -1: padding)
+  int32_t* fptr = nullptr;    // nchunks+1
+  int32_t* fmid = nullptr;    // nchunks
+  int4* fcol = nullptr;       // 2 per slot
+  double2* fval = nullptr;    // 4 per slot
+  int64_t fslots = 0;         // stored slots
+  int64_t fnnz = 0;           // far entries (without padding)
 };
 
 namespace sdb {

@@ -294,6 +294,10 @@ int sdb_matrix_create_csr(int device, int64_t n, int64_t nnz, const int64_t* ind
   } else {
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return cleanup(cuda_fail(e, "sync", __FILE__, __LINE__));
   }
+  // dense-band + far split for the probe-sliced band kernel (band.cu); a
+  // matrix without a dense symmetric band keeps the plain CSR path
+  int brc = band_build(m, s);
+  if (brc) return cleanup(brc);
   *out = m;
   return SDB_OK;
 }
@@ -411,6 +415,11 @@ void sdb_matrix_destroy(sdb_matrix* m) {
   if (m->diag) cudaFree(m->diag);
   if (m->terms) cudaFree(m->terms);
   if (m->term_w) cudaFree(m->term_w);
+  if (m->bu) cudaFree(m->bu);
+  if (m->fptr) cudaFree(m->fptr);
+  if (m->fmid) cudaFree(m->fmid);
+  if (m->fcol) cudaFree(m->fcol);
+  if (m->fval) cudaFree(m->fval);
   delete m;
 }
 

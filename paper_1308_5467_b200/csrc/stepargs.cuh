@@ -114,6 +114,29 @@ int zm_launch_pair(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, cons
                    cudaStream_t s);
 // diagonal (n) -> ghost-padded [nz][ny+4][nx+4]
 int zm_pad_diag(const sdb_matrix* m, double* padded, cudaStream_t s);
+
+// ---- probe-sliced band + far path (band.cu) --------------------------------------
+// Plan for sdb_cheb_moments on a CSR matrix with a dense symmetric band: the
+// recurrence buffers are slice-major blocks [ns][rows][S] (S probes per
+// slice, `pad` zero guard rows before and after the n_pad tile rows).
+struct BandPlan {
+  bool on = false;
+  int hb = 0;              // band half-width (kernel instantiation)
+  int S = 16;              // probe columns per slice (8 or 16)
+  int R = 128;             // rows per tile
+  int ns = 0;              // probe slices
+  int64_t ldvb = 0;        // ns * S: partials row width
+  int64_t rows = 0;        // rows per slice incl. guards
+  int64_t ntiles = 0;      // 128-row tiles per slice
+  int64_t grid = 0;        // persistent blocks (= partial rows)
+  size_t smem = 0;
+  size_t block_bytes = 0;  // one slice-major block
+};
+int band_plan(const sdb_matrix* m, int64_t n_vec, int mode, BandPlan* p);
+// probes (n x ldv row-major) -> slice-major v0b; zero the guard rows of bufA/bufB
+int band_pack(const sdb_matrix* m, const BandPlan& p, const double* probes, int64_t ldv, double* v0b, double* bufA,
+              double* bufB, cudaStream_t s);
+int band_launch_step(const sdb_matrix* m, const BandPlan& p, const StepArgs& a, bool first, int mode, cudaStream_t s);
 // probes (n x ldv) -> padded block
 int zm_pad(const sdb_matrix* m, const ZmPlan& p, const double* probes, int64_t ldv, double* padded, cudaStream_t s);
 

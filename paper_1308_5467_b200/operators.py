@@ -414,6 +414,9 @@ class DeviceMatrix:
         self.nnz = nnz
         self.format = fmt
         self.bytes_per_pass = stream_bytes  # M_A: matrix bytes one SpMM streams
+        self.band_half_width = 0
+        self.band_far_entries = 0
+        self.band_bytes_per_pass = 0
         self._finalizer = weakref.finalize(self, _destroy_handle, handle)
 
     @classmethod
@@ -455,7 +458,13 @@ class DeviceMatrix:
                                                     ctypes.byref(h)))
         info = _native.SdbMatrixInfo()
         _native.check(lib.sdb_matrix_get_info(h, ctypes.byref(info)))
-        return cls(h, device, info.n, info.nnz, info.format, info.bytes)
+        dm = cls(h, device, info.n, info.nnz, info.format, info.bytes)
+        hb, far, bpp = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+        _native.check(lib.sdb_matrix_band_info(h, ctypes.byref(hb), ctypes.byref(far), ctypes.byref(bpp)))
+        dm.band_half_width = hb.value    # dense-band + far split (band.cu); 0: plain CSR
+        dm.band_far_entries = far.value
+        dm.band_bytes_per_pass = bpp.value  # matrix bytes one 16-probe slice pass streams
+        return dm
 
 
 def _destroy_handle(h):

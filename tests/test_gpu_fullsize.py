@@ -1,14 +1,19 @@
-"""BASELINE.json's full sizes on the GPU, checked through properties that do not
-depend on size plus oracle parity on a probe subset / moment prefix:
+"""BASELINE.json's full sizes on the GPU, checked against the C oracle on probe
+subsets (draw(l) is independent of the other probes, stochastic.py:22-27, and
+moments are exact prefixes, kpm.py:49-59) plus size-independent properties:
 
-* C3 (n = 1e6, ~61M nnz CSR, KPM M = 1000, 128 Gaussian probes): zeta_0 equals
-  the host-computed mean |v|^2, |zeta_k| <= zeta_0, per-probe moments of probes
-  {0, 1} match the C oracle on the first 200 moments (the doubling steps are the
-  same; prefix property, kpm.py:49-59), DOS equals the oracle's evaluation of
-  the GPU moments (north-star tolerances: 1e-10 moments, 1e-9 DOS).
-* C5 (256^3 27-point stencil, M = 2000, 32 Rademacher probes): zeta_0 = n
-  exactly per probe, |zeta_k| <= n, direct == doubling on a prefix, and the
-  row-partitioned run (plane ranges on full-size blocks) == the whole-grid run.
+* C2 bench workload exactly (Anderson 64^3 CSR, 64 Rademacher probes, M = 500
+  doubling, Jackson, 2000 points) end to end through estimate_dos against the
+  C oracle's moments of all 64 probes and the NumPy oracle's DOS of those.
+* C3 (n = 1e6, ~61M nnz CSR, KPM M = 1000, 128 Gaussian probes, band + far
+  kernel): per-probe moments of probes {0, 1} at the FULL M = 1000 against the
+  C oracle; zeta_0 = host mean |v|^2, |zeta_k| <= zeta_0; the DOS stage fed
+  with the GPU moments against the oracle's evaluation of the same moments.
+* C5 (256^3 27-point stencil, M = 2000, 32 Rademacher probes): probes {0, 1}
+  at M = 200 against the C oracle's stencil path (pinned to its CSR path,
+  tests/test_oracle_stencil.py); zeta_0 = n exactly, |zeta_k| <= n, direct ==
+  doubling on a prefix, row-partitioned run == whole-grid run.
+Tolerances (north star): moments max|dz|/max|z| <= 1e-10, DOS max-abs <= 1e-9.
 """
 
 import numpy as np
@@ -46,11 +51,11 @@ def test_c3_full_config_properties_and_oracle_prefix(c3):
     norms = np.array([np.dot(v, v) for v in (src.draw(l) for l in range(cfg.n_vec))])
     assert rel(zpp[:, 0], norms) <= 1e-12
     assert np.all(np.abs(zpp) <= zpp[:, :1] * (1 + 1e-10))  # |T_k| <= 1 on the mapped spectrum
-    if c_oracle.available():
-        probes = np.array([src.draw(l) for l in (0, 1)])
-        ref = c_oracle.cheb_moments(mat.csr, iv.center, iv.halfwidth, 200, probes, mode="doubling", threads=2)
-        for l in (0, 1):
-            assert rel(zpp[l, :201], ref[l]) <= 1e-10
+    assert c_oracle.available()
+    probes = np.array([src.draw(l) for l in (0, 1)])
+    ref = c_oracle.cheb_moments(mat.csr, iv.center, iv.halfwidth, cfg.degree, probes, mode="doubling", threads=2)
+    for l in (0, 1):
+        assert rel(zpp[l], ref[l]) <= 1e-10
     est = sdb.estimate_dos(mat, iv, "kpm-jackson", cfg.degree, src, cfg.n_vec, grid_points=cfg.grid_points,
                            product_formula=True)
     zeta = est.params["moments"]
@@ -69,6 +74,13 @@ def test_c5_full_config_properties_and_row_partition():
     run = E.run_chebyshev(mapped, cfg.degree, src, cfg.n_vec, _native.SDB_CHEB_DOUBLING)
     zpp = run.zeta_pp.cpu().numpy()
     n = float(op.dim)
+    from oracle import c_oracle
+
+    assert c_oracle.available()
+    probes = np.array([src.draw(l) for l in (0, 1)])
+    ref = c_oracle.stencil_moments(op, iv.center, iv.halfwidth, 200, probes, mode="doubling", threads=2)
+    for l in (0, 1):
+        assert rel(zpp[l, :201], ref[l]) <= 1e-10
     assert np.all(np.isfinite(zpp))
     assert np.all(zpp[:, 0] == n)  # Rademacher probes: v.v = n exactly
     assert np.all(np.abs(zpp) <= n * (1 + 1e-10))
@@ -100,3 +112,24 @@ def test_c4_full_config_quadrature_properties():
     alpha, beta = O.lanczos_factorize(op.csr, src.draw(0), cfg.degree)[:2]
     f = sdb.lanczos_factorize(op, src.draw(0), cfg.degree)
     assert rel(f.alpha, alpha) <= 1e-10 and np.max(np.abs(f.beta - beta)) <= 1e-10 * np.max(np.abs(alpha))
+
+
+def test_c2_bench_workload_end_to_end():
+    """bench.py --config C2 exactly: CSR input (detected stencil), 64 Rademacher
+    probes, M = 500 product formula, Jackson, 2000 points."""
+    from oracle import c_oracle
+
+    op = W.build_matrix("C2")
+    mat = sdb.SparseSymmetricMatrix(csr=op.csr)
+    iv = W.gershgorin_interval(mat)
+    cfg = W.CONFIGS["C2"]
+    src = sdb.ProbeVectorSource(cfg.probe_kind, seed=0, dim=mat.dim)
+    est = sdb.estimate_dos(mat, iv, "kpm-jackson", cfg.degree, src, cfg.n_vec, grid_points=cfg.grid_points,
+                           product_formula=True)
+    probes = np.array([src.draw(l) for l in range(cfg.n_vec)])
+    ref = c_oracle.cheb_moments(mat.csr, iv.center, iv.halfwidth, cfg.degree, probes, mode="doubling")
+    zeta = ref.mean(axis=0)
+    assert rel(est.params["moments"], zeta) <= 1e-10
+    _, dens = O.evaluate_kpm_dos(O.moments_to_coefficients(zeta, mat.dim, "jackson"), iv.halfwidth,
+                                 O.unit_grid(cfg.grid_points))
+    assert np.max(np.abs(est.density - dens)) <= 1e-9
