@@ -572,11 +572,10 @@ static void lz_upj_launch(dim3 grid, const double* basis, const double* wsrc, do
                           int64_t n,
                           int64_t ldv, int64_t nrb, double* part, cudaStream_t s) {
   const size_t smem = (size_t)KM * TG * kZcs * sizeof(double2);
-  static bool attr = false;
-  if (!attr && smem > 48 * 1024) {
-    cudaFuncSetAttribute(lz_update_proj<KM, RW, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+  // function attributes are per device: set on every launch (cheap); a failure
+  // surfaces through the launch check that follows
+  if (smem > 48 * 1024)
+    (void)cudaFuncSetAttribute(lz_update_proj<KM, RW, TG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   lz_update_proj<KM, RW, TG><<<grid, kZcs * TG, smem, s>>>(basis, wsrc, w, h, j, n, ldv, nrb, part);
 }
 

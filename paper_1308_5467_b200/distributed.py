@@ -85,18 +85,30 @@ def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=
     import torch
     import torch.distributed as dist
 
-    from .lanczos import _pool_device, _blur_device, lanczos_quadrature_device
+    from .lanczos import _pool_device, _blur_device, _raise_for_status, lanczos_quadrature_device
+    from .operators import resolve
 
     if method not in SHARDED_METHODS:
         raise ValueError(f"sharded estimates support {SHARDED_METHODS}")
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
+    # argument checks come before any work and depend only on the arguments,
+    # so every rank raises together (a rank raising alone would leave its
+    # peers blocked in the gather)
+    if n_vec < world:
+        raise ValueError(f"every rank needs at least one probe (n_vec={n_vec}, world size {world})")
     start, count = shard_range(n_vec, world, rank)
-    if count < 1:
-        raise ValueError("every rank needs at least one probe")
     dev = torch.cuda.current_device()
     shifted = _ShiftedSource(source, start)
     counter = MatvecCounter(as_operator(matrix))
+    user_counters = resolve(counter).counters[1:] if len(resolve(counter).counters) > 1 else []
+
+    def credit(total):
+        # the caller's own MatvecCounter layers see the whole job's MATVECs,
+        # as on the single-device paths (E.credit_counters)
+        counter.count = int(total)
+        for c in user_counters:
+            c.count += int(total)
     if product_formula and method not in ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb"):
         raise ValueError("the product formula only applies to Chebyshev moments")
     if method in ("dgl", "lanczos") and (sigma is None or not sigma > 0):
@@ -114,7 +126,7 @@ def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=
         m1, g = degree + 1, len(grid)
         if packed[-1] != 0.0 or not np.all(np.isfinite(packed[:m1])):
             raise NumericalFailure(E.SPECTRUM_ESCAPE_HINT)
-        counter.count += n_vec * run.matvecs_per_probe
+        credit(n_vec * run.matvecs_per_probe)
         est = SpectralDensityEstimate.from_parts(grid, packed[m1:m1 + g], interval.from_unit(grid),
                                                  packed[m1 + g:m1 + 2 * g], interval,
                                                  method=method, params={"degree": degree, "moments": packed[:m1]})
@@ -133,7 +145,7 @@ def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=
         packed = torch.cat([zeta_dev, flag.to(torch.float64)]).cpu().numpy()
         if packed[-1] != 0.0 or not np.all(np.isfinite(packed[:-1])):
             raise NumericalFailure(E.SPECTRUM_ESCAPE_HINT)
-        counter.count += n_vec * run.matvecs_per_probe
+        credit(n_vec * run.matvecs_per_probe)
         moments = K.MomentSequence(zeta=packed[:-1], degree=degree, n_vec=n_vec,
                                    basis="legendre" if legendre else "chebyshev", n=run.n)
         grid = unit_grid(grid_points)
@@ -153,11 +165,14 @@ def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=
             eta = interval.width / (2.0 * len(grid))
         if not eta > 0:
             raise ValueError("eta must be positive")
-        _, alpha, beta, sd, st = lanczos_tridiagonals_device(counter, degree, shifted, count, device=dev)
-        a_all = gather_probe_rows(alpha, n_vec, group).contiguous()
-        b_all = gather_probe_rows(beta, n_vec, group).contiguous()
+        _, alpha, beta, sd, st = lanczos_tridiagonals_device(counter, degree, shifted, count, device=dev,
+                                                             check=False)
+        # status rows first: every rank raises the same first error in probe order
         sds = gather_probe_rows(sd.view(-1, 1).to(torch.float64), n_vec, group).view(-1).to(torch.int32)
         sts = gather_probe_rows(st.view(-1, 1).to(torch.float64), n_vec, group).view(-1).to(torch.int32)
+        _raise_for_status(sts.cpu().numpy(), sds.cpu().numpy())
+        a_all = gather_probe_rows(alpha, n_vec, group).contiguous()
+        b_all = gather_probe_rows(beta, n_vec, group).contiguous()
         stream = E.stream_ptr(dev)
         g = E.to_device(grid, dev)
         dens = torch.empty_like(g)
@@ -166,7 +181,7 @@ def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=
         _native.call("sdb_haydock", E.ptr(a_all), E.ptr(b_all), E.ptr(sds), E.ptr(sts), n_vec, degree, E.ptr(g),
                      g.numel(), float(eta), E.ptr(dens), E.ptr(tpts), E.ptr(trunc), stream)
         packed = torch.cat([dens, trunc]).cpu().numpy()
-        counter.count = int(sds.sum().item())
+        credit(sds.sum().item())
         est = SpectralDensityEstimate.from_original(
             grid, packed[:-1], interval, method="haydock",
             params={"M": degree, "n_vec": n_vec, "eta": eta, "truncation_indicator": float(packed[-1])})
@@ -174,13 +189,17 @@ def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=
         from .lanczos import DEFAULT_MERGE_RTOL, _cdos_device
 
         grid = interval_grid(interval, grid_points)
-        _, theta, tau2, sd, _ = lanczos_quadrature_device(counter, degree, shifted, count, device=dev)
+        st_box = []
+        _, theta, tau2, sd, _ = lanczos_quadrature_device(counter, degree, shifted, count, device=dev,
+                                                          status_out=st_box)
+        sds = gather_probe_rows(sd.view(-1, 1).to(torch.float64), n_vec, group).view(-1).to(torch.int32)
+        sts = gather_probe_rows(st_box[0].view(-1, 1).to(torch.float64), n_vec, group).view(-1).to(torch.int32)
+        _raise_for_status(sts.cpu().numpy(), sds.cpu().numpy())
         th = gather_probe_rows(theta, n_vec, group)
         tw = gather_probe_rows(tau2, n_vec, group)
-        sds = gather_probe_rows(sd.view(-1, 1).to(torch.float64), n_vec, group).view(-1).to(torch.int32)
         stream = E.stream_ptr(dev)
         nodes, weights = _pool_device(th, tw, sds, n_vec, dev, stream)
-        counter.count = int(sds.sum().item())
+        credit(sds.sum().item())
         if method == "lanczos":
             dens = _blur_device(nodes, weights, E.to_device(grid, dev), "gaussian", sigma, 1.0, dev, stream)
             density = dens.cpu().numpy()

@@ -264,11 +264,14 @@ def blur_nodes(theta, weights, grid, kernel, block=512, device=None):
         return out.cpu().numpy().reshape(grid.shape)
 
 
-def lanczos_quadrature_device(op, steps, source, n_vec, reorth="full", device=None, probes=None):
+def lanczos_quadrature_device(op, steps, source, n_vec, reorth="full", device=None, probes=None, status_out=None):
     """All probes' (theta, tau2, steps_done) on device, batched in lock-step.
 
     Returns (res, theta (n_vec, steps), tau2, steps_done, h2d_bytes).
-    Raises like the reference on zero starting vectors / non-finite runs.
+    Raises like the reference on zero starting vectors / non-finite runs;
+    with ``status_out`` (a list) the per-probe status tensor is appended
+    instead and the caller raises (the sharded path gathers it first, so
+    every rank raises the same error).
     """
     torch = E._torch()
     device = E.require_cuda(device)
@@ -296,6 +299,9 @@ def lanczos_quadrature_device(op, steps, source, n_vec, reorth="full", device=No
             tau2[start:start + count] = tw
             sd_all[start:start + count] = out.steps_done
             st_all[start:start + count] = out.status
+        if status_out is not None:
+            status_out.append(st_all)
+            return res, theta, tau2, sd_all, h2d
         status = st_all.cpu().numpy()
         sd = sd_all.cpu().numpy()
     _raise_for_status(status, sd)
@@ -333,8 +339,10 @@ def lanczos_dos(op, interval, steps, source, n_vec, sigma, grid=None, threads=No
 # probe's continued fraction and truncation diagnostic per grid point.
 
 
-def lanczos_tridiagonals_device(op, steps, source, n_vec, reorth="full", device=None, probes=None):
-    """All probes' (alpha, beta, steps_done, status) on device (sdb_lanczos layout)."""
+def lanczos_tridiagonals_device(op, steps, source, n_vec, reorth="full", device=None, probes=None, check=True):
+    """All probes' (alpha, beta, steps_done, status) on device (sdb_lanczos layout).
+
+    ``check=False`` leaves raising on the status row to the caller."""
     torch = E._torch()
     device = E.require_cuda(device)
     res = resolve(op)
@@ -358,6 +366,8 @@ def lanczos_tridiagonals_device(op, steps, source, n_vec, reorth="full", device=
             beta[start:start + count] = out.beta
             sd_all[start:start + count] = out.steps_done
             st_all[start:start + count] = out.status
+        if not check:
+            return res, alpha, beta, sd_all, st_all
         status = st_all.cpu().numpy()
         sd = sd_all.cpu().numpy()
     _raise_for_status(status, sd)

@@ -80,3 +80,43 @@ def test_probe_shard_gather_matches_single_process(n_vec):
     for _, rows, zeta in results:
         np.testing.assert_array_equal(rows, ref)  # probe order preserved
         np.testing.assert_array_equal(zeta, O.average_moments(ref))  # GPU-count independent
+
+
+def _raise_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1308_5467_b200 as sdb
+        from paper_1308_5467_b200 import workloads as W
+        from paper_1308_5467_b200.distributed import estimate_dos_sharded
+
+        op = W.anderson_3d(4)
+        iv = W.gershgorin_interval(op)
+        src = sdb.ProbeVectorSource("rademacher", seed=0, dim=op.dim)
+        try:
+            estimate_dos_sharded(op, iv, "kpm-jackson", 10, src, 1)  # one probe, two ranks
+            out_q.put((rank, "no error"))
+        except ValueError as exc:
+            out_q.put((rank, str(exc)))
+        dist.barrier()  # both ranks are still in step: nobody is stuck in a gather
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fewer_probes_than_ranks_raises_on_every_rank():
+    """A rank without probes must not raise alone while its peers wait in the
+    all-gather: the check depends only on the arguments, so all ranks raise."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_raise_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(q.get(timeout=120) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert set(results) == {0, 1}
+    for msg in results.values():
+        assert "at least one probe" in msg
