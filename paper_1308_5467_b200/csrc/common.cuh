@@ -87,18 +87,17 @@ struct sdb_matrix {
   int shape = 0;              // SDB_SHAPE_*: specialised grid kernel available
   int zghost = 0;             // z-slab of a row partition (no z wrap, ghost planes)
   // band + far split of a CSR matrix (band.cu): the dense band |i-j| <= hb as
-  // symmetric upper diagonals, the rest (far entries) in SELL-8 slots
+  // symmetric upper diagonals, the rest (far entries) as SELL-4-sigma streams
   int hb = 0;                 // 0: no split
   int64_t ustride = 0;        // doubles per diagonal of bu
-  double* bu = nullptr;       // [hb+1][ustride]: bu[d*ustride + kBandPad(hb) + i] = A[i][i+d]
-  // far entries, SELL-8: chunk c = rows 8c..8c+7 holds slots [fptr[c], fmid[c])
-  // (lower segments) and [fmid[c], fptr[c+1]) (upper segments); slot s stores
-  // one entry per row of the chunk at fcol/fval[8s + r] (column -1: padding)
-  int32_t* fptr = nullptr;    // nchunks+1
-  int32_t* fmid = nullptr;    // nchunks
-  int4* fcol = nullptr;       // 2 per slot
-  double2* fval = nullptr;    // 4 per slot
-  int64_t fslots = 0;         // stored slots
+  double* bu = nullptr;       // [hb+1][ustride]: bu[d*ustride + band_pad(hb) + i] = A[i][i+d]
+  // far entries: per 128-row tile the rows are sorted by far count (sigma =
+  // 128), cut into 4-row chunks (C = 4) and dealt to 16 streams; a stream is a
+  // run of 208-byte batch records (4 slots x 4 rows: columns, values, chunk /
+  // tile end flags, the chunk's local row ids), see band.cu
+  int2* fhdr = nullptr;       // [ntiles][16]: (first record, records) of a stream
+  uint4* frec = nullptr;      // records, 13 x 16 B each
+  int64_t frecs = 0;          // stored records
   int64_t fnnz = 0;           // far entries (without padding)
 };
 

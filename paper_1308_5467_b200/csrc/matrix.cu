@@ -416,10 +416,8 @@ void sdb_matrix_destroy(sdb_matrix* m) {
   if (m->terms) cudaFree(m->terms);
   if (m->term_w) cudaFree(m->term_w);
   if (m->bu) cudaFree(m->bu);
-  if (m->fptr) cudaFree(m->fptr);
-  if (m->fmid) cudaFree(m->fmid);
-  if (m->fcol) cudaFree(m->fcol);
-  if (m->fval) cudaFree(m->fval);
+  if (m->fhdr) cudaFree(m->fhdr);
+  if (m->frec) cudaFree(m->frec);
   delete m;
 }
 
