@@ -63,8 +63,23 @@ def kpm_dos_device(mapped, degree, source, n_vec, damping, grid, product_formula
 
 
 def estimate_dos(matrix, interval, method, degree, source, n_vec, sigma=None, eta=None,
-                 grid_points=DEFAULT_GRID_POINTS, threads=None, product_formula=False, device=None):
-    """Run one estimator on the GPU; params carry the MATVEC count (compare.py:82-141)."""
+                 grid_points=DEFAULT_GRID_POINTS, threads=None, product_formula=False, device=None, devices=None):
+    """Run one estimator on the GPU; params carry the MATVEC count (compare.py:82-141).
+
+    ``devices=[0, 1, ...]`` shards the probes over several GPUs of this
+    process (one contiguous probe range, host thread and stream per entry;
+    the matrix is replicated); the per-probe moment / Ritz / tridiagonal rows
+    are gathered on ``devices[0]`` in probe order and evaluated there, so the
+    call keeps the reference's single-process signature.  Per-probe results
+    do not depend on the sharding beyond the rounding of their dot-product
+    reduction trees (<= 1e-13 relative).
+    """
+    if devices is not None:
+        if device is not None:
+            raise ValueError("pass either device or devices")
+        device = [int(d) for d in devices]
+        if not device:
+            raise ValueError("devices must name at least one CUDA device")
     if method not in ALL_METHODS:
         raise ValueError(f"unknown method {method!r}, expected one of {ALL_METHODS}")
     if product_formula and method not in CHEBYSHEV_METHODS:
@@ -127,6 +142,8 @@ def estimate_dos(matrix, interval, method, degree, source, n_vec, sigma=None, et
         "matvec_count": counter.count,
         "wall_time_s": time.perf_counter() - start,
     })
+    if devices is not None:
+        est.params["devices"] = list(device)
     if sigma is not None:
         est.params.setdefault("sigma", sigma)
     if product_formula:

@@ -24,11 +24,7 @@ from .operators import MatvecCounter, apply_spectral_map, as_operator
 SHARDED_METHODS = ("kpm", "kpm-jackson", "spectroscopic", "delta-cheb", "kpml", "dgl", "lanczos", "haydock", "cdos")
 
 
-def shard_range(n_vec, world, rank):
-    """Contiguous probe range of ``rank``: sizes differ by at most one."""
-    base, extra = divmod(n_vec, world)
-    start = rank * base + min(rank, extra)
-    return start, base + (1 if rank < extra else 0)
+shard_range = E.shard_range
 
 
 def gather_probe_rows(rows, n_vec, group=None):
@@ -58,22 +54,7 @@ def all_gather_probe_moments(zeta_pp, world, group=None):
     return gather_probe_rows(zeta_pp, zeta_pp.shape[0] * world, group)
 
 
-class _ShiftedSource:
-    """Probe i of this view is probe start+i of the underlying source."""
-
-    def __init__(self, src, start):
-        self.src, self.start, self.dim = src, start, src.dim
-        self.kind = getattr(src, "kind", None)
-        if hasattr(src, "draw_block_signs"):
-            self.draw_block_signs = lambda s, c: src.draw_block_signs(self.start + s, c)
-
-    def draw(self, i):
-        return self.src.draw(self.start + i)
-
-    def draw_block(self, start, count):
-        from .stochastic import draw_block
-
-        return draw_block(self.src, self.start + start, count)
+_ShiftedSource = E.ShiftedSource
 
 
 def estimate_dos_sharded(matrix, interval, method, degree, source, n_vec, sigma=None, grid_points=DEFAULT_GRID_POINTS,

@@ -5,7 +5,9 @@ arithmetic on the hot path runs in the kernels of ``libspecdens_b200.so``.
 """
 
 import ctypes
+import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
@@ -28,13 +30,24 @@ def _torch():
     return torch
 
 
+def is_device_list(device):
+    """``device`` may be one CUDA device index or a sequence of them (probe sharding)."""
+    return isinstance(device, (list, tuple))
+
+
 def require_cuda(device=None):
+    """The CUDA device to compute on (for a device list: its first entry,
+    where the sharded per-probe rows are gathered and evaluated)."""
     torch = _torch()
     if not torch.cuda.is_available():
         raise RuntimeError(
             "paper_1308_5467_b200 needs a CUDA device (sm_100a); no GPU is visible and there is no CPU fallback"
         )
     _native.load()
+    if is_device_list(device):
+        if not device:
+            raise ValueError("empty device list")
+        device = device[0]
     if device is None:
         device = torch.cuda.current_device()
     return int(device)
@@ -111,23 +124,35 @@ def pack_device_probes(probes_t, device, stream):
 
 
 class Workspace:
-    """Grow-only device scratch buffer (one per device)."""
+    """Grow-only device scratch buffers, one per (device, stream).
 
-    _per_device = {}
+    Work on a stream is ordered, so successive calls on the same stream may
+    share a buffer; calls on different streams (other host threads, the
+    shards of a multi-device estimate) each get their own and cannot race.
+    """
+
+    _lock = threading.Lock()
+    _buffers = {}
 
     @classmethod
     def get(cls, device, nbytes):
         torch = _torch()
-        buf = cls._per_device.get(device)
-        if buf is None or buf.numel() < nbytes:
-            cls._per_device.pop(device, None)
-            buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
-            cls._per_device[device] = buf
+        key = (int(device), int(torch.cuda.current_stream(device).cuda_stream))
+        with cls._lock:
+            buf = cls._buffers.get(key)
+            if buf is None or buf.numel() < nbytes:
+                cls._buffers.pop(key, None)
+                buf = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=device)
+                cls._buffers[key] = buf
         return buf
 
     @classmethod
-    def release(cls):
-        cls._per_device.clear()
+    def release(cls, device=None, stream=None):
+        """Drop the buffers (all, or those of one device / one stream)."""
+        with cls._lock:
+            for key in list(cls._buffers):
+                if (device is None or key[0] == int(device)) and (stream is None or key[1] == int(stream)):
+                    del cls._buffers[key]
 
 
 # ---------------------------------------------------------------------------
@@ -145,14 +170,96 @@ class MomentRun:
     dm: object
 
 
-def run_chebyshev(op, degree, source, n_vec, mode, device=None, probes=None, time_steps=False):
-    """Per-probe Chebyshev moments of the resolved operator on one device.
+# ---------------------------------------------------------------------------
+# probe sharding over several devices of one process (probe
+# recurrences are independent units)
 
+
+def shard_range(n_vec, world, rank):
+    """Contiguous probe range of shard ``rank``: sizes differ by at most one."""
+    base, extra = divmod(n_vec, world)
+    start = rank * base + min(rank, extra)
+    return start, base + (1 if rank < extra else 0)
+
+
+class ShiftedSource:
+    """Probe i of this view is probe start+i of the underlying source."""
+
+    def __init__(self, src, start):
+        self.src, self.start, self.dim = src, start, src.dim
+        self.kind = getattr(src, "kind", None)
+        if hasattr(src, "draw_block_signs"):
+            self.draw_block_signs = lambda s, c: src.draw_block_signs(self.start + s, c)
+
+    def draw(self, i):
+        return self.src.draw(self.start + i)
+
+    def draw_block(self, start, count):
+        return draw_block(self.src, self.start + start, count)
+
+
+def run_sharded(fn, n_vec, devices, source=None, probes=None):
+    """Run ``fn(shard_source, shard_probes, count, device)`` for every shard.
+
+    Shard r is the contiguous probe range ``shard_range(n_vec, len(devices),
+    r)`` on ``devices[r]`` (a device may appear several times), each on its
+    own host thread and CUDA stream, so the shards of one device queue behind
+    each other while different devices run concurrently.  Returns the shard
+    results in probe order; every shard's stream has been synchronised.
+    """
+    torch = _torch()
+    devices = [int(d) for d in devices][:max(1, n_vec)]
+    world = len(devices)
+
+    def work(r):
+        start, count = shard_range(n_vec, world, r)
+        d = devices[r]
+        with torch.cuda.device(d):
+            stream = torch.cuda.Stream(device=d)
+            with torch.cuda.stream(stream):
+                src = ShiftedSource(source, start) if source is not None else None
+                pr = None
+                if probes is not None:
+                    pr = probes[start:start + count]
+                    if pr.device.index != d:
+                        pr = pr.to(d)
+                out = fn(src, pr, count, d)
+            stream.synchronize()
+            Workspace.release(d, stream.cuda_stream)
+        return out
+
+    if world == 1:
+        return [work(0)]
+    with ThreadPoolExecutor(max_workers=world) as ex:
+        return list(ex.map(work, range(world)))
+
+
+def run_chebyshev(op, degree, source, n_vec, mode, device=None, probes=None, time_steps=False):
+    """Per-probe Chebyshev moments of the resolved operator.
+
+    ``device``: one CUDA device, or a list of devices: the probes are then
+    sharded over them (one contiguous range per list entry, one stream each)
+    and the per-probe rows gathered on the first device, in probe order.
     ``probes`` optionally supplies an on-device (n_vec, n) tensor instead of
     drawing from ``source`` (used by the benchmark's device-resident leg and
     the multi-GPU shard, which pass their own slice).
     """
     torch = _torch()
+    if is_device_list(device):
+        primary = require_cuda(device)
+        res = resolve(op)
+        for d in sorted(set(int(x) for x in device)):  # one upload per device, before the shards start
+            with torch.cuda.device(d):
+                device_matrix(res.base, d, stream_ptr(d))
+                torch.cuda.current_stream(d).synchronize()
+        runs = run_sharded(lambda src, pr, count, d: run_chebyshev(op, degree, src, count, mode, device=d, probes=pr,
+                                                                   time_steps=time_steps),
+                           n_vec, device, source=source if probes is None else None, probes=probes)
+        with torch.cuda.device(primary):
+            zeta_pp = torch.cat([r.zeta_pp.to(primary) for r in runs], dim=0)
+        return MomentRun(zeta_pp=zeta_pp, n=runs[0].n, resolved=runs[0].resolved,
+                         matvecs_per_probe=runs[0].matvecs_per_probe, step_ms=max(r.step_ms for r in runs),
+                         h2d_bytes=sum(r.h2d_bytes for r in runs), dm=runs[0].dm)
     device = require_cuda(device)
     res = resolve(op)
     n = res.dim

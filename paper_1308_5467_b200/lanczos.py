@@ -101,6 +101,15 @@ def _raise_for_status(status, steps_done, first_index=0):
     raise NumericalFailure(f"non-finite Lanczos recurrence at step {int(steps_done[l])}")
 
 
+def _upload_everywhere(base, devices):
+    """One matrix upload per distinct device, before any shard thread starts."""
+    torch = E._torch()
+    for d in sorted(set(int(x) for x in devices)):
+        with torch.cuda.device(d):
+            device_matrix(base, d, E.stream_ptr(d))
+            torch.cuda.current_stream(d).synchronize()
+
+
 def _batch_size(n, steps, n_vec):
     per_col = 8 * steps * n
     cap = max(1, BASIS_BUDGET_BYTES // max(per_col, 1))
@@ -274,6 +283,30 @@ def lanczos_quadrature_device(op, steps, source, n_vec, reorth="full", device=No
     every rank raises the same error).
     """
     torch = E._torch()
+    if E.is_device_list(device):  # probe shards, one per list entry; rows gathered on the first device
+        primary = E.require_cuda(device)
+        res = resolve(op)
+        _check_args(reorth, steps, res.dim)
+        _upload_everywhere(res.base, device)
+
+        def shard(src, pr, count, d):
+            box = []
+            out = lanczos_quadrature_device(op, steps, src, count, reorth=reorth, device=d, probes=pr,
+                                            status_out=box)
+            return out, box[0]
+
+        parts = E.run_sharded(shard, n_vec, device, source=source if probes is None else None, probes=probes)
+        with torch.cuda.device(primary):
+            theta = torch.cat([p[0][1].to(primary) for p in parts], dim=0)
+            tau2 = torch.cat([p[0][2].to(primary) for p in parts], dim=0)
+            sd_all = torch.cat([p[0][3].to(primary) for p in parts], dim=0)
+            st_all = torch.cat([p[1].to(primary) for p in parts], dim=0)
+            h2d = sum(p[0][4] for p in parts)
+            if status_out is not None:
+                status_out.append(st_all)
+                return res, theta, tau2, sd_all, h2d
+            _raise_for_status(st_all.cpu().numpy(), sd_all.cpu().numpy())
+        return res, theta, tau2, sd_all, h2d
     device = E.require_cuda(device)
     res = resolve(op)
     n = res.dim
@@ -316,8 +349,8 @@ def lanczos_dos(op, interval, steps, source, n_vec, sigma, grid=None, threads=No
         grid = interval_grid(interval, DEFAULT_GRID_POINTS)
     grid = np.asarray(grid, dtype=float)
     torch = E._torch()
-    device = E.require_cuda(device)
-    res, theta, tau2, sd, _ = lanczos_quadrature_device(op, steps, source, n_vec, reorth=reorth, device=device)
+    devices, device = device, E.require_cuda(device)
+    res, theta, tau2, sd, _ = lanczos_quadrature_device(op, steps, source, n_vec, reorth=reorth, device=devices)
     with torch.cuda.device(device):
         stream = E.stream_ptr(device)
         nodes, weights = _pool_device(theta, tau2, sd, n_vec, device, stream)
@@ -344,6 +377,19 @@ def lanczos_tridiagonals_device(op, steps, source, n_vec, reorth="full", device=
 
     ``check=False`` leaves raising on the status row to the caller."""
     torch = E._torch()
+    if E.is_device_list(device):
+        primary = E.require_cuda(device)
+        res = resolve(op)
+        _check_args(reorth, steps, res.dim)
+        _upload_everywhere(res.base, device)
+        parts = E.run_sharded(lambda src, pr, count, d: lanczos_tridiagonals_device(
+            op, steps, src, count, reorth=reorth, device=d, probes=pr, check=False), n_vec, device,
+            source=source if probes is None else None, probes=probes)
+        with torch.cuda.device(primary):
+            alpha, beta, sd_all, st_all = (torch.cat([p[k].to(primary) for p in parts], dim=0) for k in (1, 2, 3, 4))
+            if check:
+                _raise_for_status(st_all.cpu().numpy(), sd_all.cpu().numpy())
+        return res, alpha, beta, sd_all, st_all
     device = E.require_cuda(device)
     res = resolve(op)
     n = res.dim
@@ -426,8 +472,8 @@ def haydock_dos(op, interval, steps, source, n_vec, eta=None, grid=None, threads
     if not eta > 0:
         raise ValueError("eta must be positive")
     torch = E._torch()
-    device = E.require_cuda(device)
-    res, alpha, beta, sd, st = lanczos_tridiagonals_device(op, steps, source, n_vec, reorth=reorth, device=device)
+    devices, device = device, E.require_cuda(device)
+    res, alpha, beta, sd, st = lanczos_tridiagonals_device(op, steps, source, n_vec, reorth=reorth, device=devices)
     with torch.cuda.device(device):
         stream = E.stream_ptr(device)
         g = E.to_device(grid, device)
@@ -520,8 +566,8 @@ def cdos_dos(op, interval, steps, source, n_vec, grid=None, threads=None, reorth
         grid = interval_grid(interval, DEFAULT_GRID_POINTS)
     grid = np.asarray(grid, dtype=float)
     torch = E._torch()
-    device = E.require_cuda(device)
-    res, theta, tau2, sd, _ = lanczos_quadrature_device(op, steps, source, n_vec, reorth=reorth, device=device)
+    devices, device = device, E.require_cuda(device)
+    res, theta, tau2, sd, _ = lanczos_quadrature_device(op, steps, source, n_vec, reorth=reorth, device=devices)
     with torch.cuda.device(device):
         stream = E.stream_ptr(device)
         nodes_p, weights_p = _pool_device(theta, tau2, sd, n_vec, device, stream)  # sorted by theta

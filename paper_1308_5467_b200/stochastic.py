@@ -33,7 +33,10 @@ class ProbeVectorSource:
     seed: int
     dim: int
     stream: int = 0
+    # drawn blocks kept in pinned host memory (a pure-function cache: the value
+    # object stays immutable for every observer); guarded by _lock
     _cache: dict = field(default_factory=dict, compare=False, repr=False, hash=False)
+    _lock: object = field(default_factory=threading.Lock, compare=False, repr=False, hash=False)
 
     def __post_init__(self):
         if self.kind not in PROBE_KINDS:
@@ -74,7 +77,8 @@ class ProbeVectorSource:
         import torch
 
         key = ("signs", start, count)
-        hit = self._cache.get(key)
+        with self._lock:
+            hit = self._cache.get(key)
         if hit is not None:
             return hit
         nb = (int(self.dim) + 7) // 8
@@ -92,10 +96,7 @@ class ProbeVectorSource:
         else:
             for i in range(count):
                 one(i)
-        self._cache.pop(key, None)
-        for k in [k for k in self._cache if isinstance(k, tuple) and k and k[0] == "signs"]:
-            self._cache.pop(k)
-        self._cache[key] = out
+        _cache_put(self._cache, self._lock, key, out)
         return out
 
     def draw_block(self, start, count, out=None):
@@ -103,7 +104,7 @@ class ProbeVectorSource:
 
         Uses a one-entry cache of pinned host memory (see module doc).
         """
-        return _draw_block(self, start, count, out, cache=self._cache)
+        return _draw_block(self, start, count, out, cache=self._cache, lock=self._lock)
 
 
 _pool_lock = threading.Lock()
@@ -122,12 +123,26 @@ def _draw_rows(source, start, count, out):
             one(i)
 
 
-def _draw_block(source, start, count, out, cache=None):
+def _cache_put(cache, lock, key, block):
+    """Insert a drawn block; the oldest blocks go once the pinned budget is exceeded."""
+    with lock:
+        cache.pop(key, None)
+        cache[key] = block
+        total = sum(b.numel() * b.element_size() for b in cache.values())
+        for k in list(cache):
+            if total <= PINNED_CACHE_BYTES or k == key:
+                break
+            b = cache.pop(k)
+            total -= b.numel() * b.element_size()
+
+
+def _draw_block(source, start, count, out, cache=None, lock=None):
     import torch
 
     key = ("values", start, count)
     if cache is not None:
-        hit = cache.get(key)
+        with lock:
+            hit = cache.get(key)
         if hit is not None:
             if out is not None:
                 out.copy_(hit)
@@ -139,9 +154,7 @@ def _draw_block(source, start, count, out, cache=None):
         out = torch.empty((count, int(source.dim)), dtype=torch.float64, pin_memory=pin)
     _draw_rows(source, start, count, out.numpy())
     if cache is not None and nbytes <= PINNED_CACHE_BYTES:
-        for k in [k for k in cache if isinstance(k, tuple) and k and k[0] == "values"]:
-            cache.pop(k)
-        cache[key] = out
+        _cache_put(cache, lock, key, out)
     return out
 
 
