@@ -41,30 +41,34 @@ class SparseSymmetricMatrix:
 
     @classmethod
     def from_coo(cls, n, rows, cols, vals, symmetric_storage=False):
-        rows = np.asarray(rows, dtype=np.int64)
-        cols = np.asarray(cols, dtype=np.int64)
-        vals = np.asarray(vals, dtype=np.float64)
-        if rows.size and (rows.min() < 0 or cols.min() < 0 or rows.max() >= n or cols.max() >= n):
-            raise ValueError("coordinate index out of range")
-        if symmetric_storage:
-            off = rows != cols
-            rows, cols = np.concatenate([rows, cols[off]]), np.concatenate([cols, rows[off]])
-            vals = np.concatenate([vals, vals[off]])
-        a = sp.coo_array((vals, (rows, cols)), shape=(n, n)).tocsr()
-        a.sum_duplicates()
-        mat = cls(csr=a, symmetric_storage=symmetric_storage)
-        if not mat.is_symmetric():
+        """CSR from coordinate triplets with duplicates summed (contract of
+        matrix.py:47-70): one stored triangle is mirrored when
+        ``symmetric_storage`` is set, otherwise the triplets must already
+        describe an exactly symmetric matrix."""
+        i, j = (np.asarray(x, dtype=np.int64) for x in (rows, cols))
+        v = np.asarray(vals, dtype=np.float64)
+        for idx in (i, j):
+            if idx.size and not (0 <= idx.min() and idx.max() < n):
+                raise ValueError("coordinate index out of range")
+        if symmetric_storage:  # append the transposed strict triangle after the given entries
+            strict = np.flatnonzero(i != j)
+            i, j, v = np.r_[i, j[strict]], np.r_[j, i[strict]], np.r_[v, v[strict]]
+        csr = sp.coo_array((v, (i, j)), shape=(n, n)).tocsr()
+        csr.sum_duplicates()
+        out = cls(csr=csr, symmetric_storage=symmetric_storage)
+        if not out.is_symmetric():
             raise ValueError("matrix data is not symmetric")
-        return mat
+        return out
 
     @classmethod
     def from_dense(cls, a):
-        a = np.asarray(a, dtype=float)
-        if a.ndim != 2 or a.shape[0] != a.shape[1]:
+        """CSR of an exactly symmetric dense array (matrix.py:72-79)."""
+        dense = np.asarray(a, dtype=float)
+        if dense.ndim != 2 or dense.shape[0] != dense.shape[1]:
             raise ValueError("dense input must be square")
-        if not np.array_equal(a, a.T):
+        if (dense != dense.T).any():
             raise ValueError("dense input must be exactly symmetric")
-        return cls(csr=sp.csr_array(a))
+        return cls(csr=sp.csr_array(dense))
 
     @property
     def n(self):
