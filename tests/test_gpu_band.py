@@ -2,12 +2,13 @@
 
 * The split is made at upload only for CSR matrices with a dense, bit-exactly
   symmetric band and sorted rows; otherwise the plain CSR kernel runs.
-* Its w is bit-identical to the CSR kernel's (same fma chain per row), so the
-  moments agree with the CSR kernel's to reduction-order rounding, and with the
-  C oracle (csr_matvec order, kpm.py:96-107 / :174-189) within the north-star
-  1e-10 (max|dz|/max|z|).
+* A row's sum runs far entries (column order) then the band, the CSR kernel in
+  pure column order: w agrees to rounding, the moments with the CSR kernel's
+  to 1e-13 and with the C oracle (csr_matvec order, kpm.py:96-107 / :174-189)
+  within the north-star 1e-10 (max|dz|/max|z|).
 * Edge cases: n not a multiple of the 128-row tile, probe counts that are not a
-  multiple of the 16-column slice (1, 20, 130), every moment mode.
+  multiple of the 16-column slice (1, 20, 130), every moment mode, a narrow
+  band (half-width 8) on a matrix of a few tiles.
 """
 
 import os

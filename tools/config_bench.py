@@ -1,11 +1,16 @@
 """Time every BASELINE config on one GPU (device-resident probes, CUDA events).
 
-  python tools/config_bench.py [C1 C2 C3 C4 C5] [--format csr|stencil] [--reps 3]
+  python tools/config_bench.py [C1 C2 C3 C4 C5] [--format csr|stencil] [--reps 3] [--cpu]
 
 Prints one JSON line per config: wall time of one full estimate, GNNZ-vec/s
 (nnz * n_vec * M / t), the step-kernel roofline fraction (KPM) or the whole
-Lanczos run's algorithmic-bytes rate (Lanczos).  Not the headline bench
-(bench.py measures C2); used for DESIGN.md and profiles/.
+Lanczos run's algorithmic-bytes rate (Lanczos).  With --cpu every line also
+carries the CPU baseline timed on this box's host cores (BASELINE.md §2,
+SURVEY §8d): the C restatement of the reference recurrence on all host
+threads for the KPM configs (C5 through its stencil path), the NumPy/SciPy
+restatement of ``lanczos_dos`` for C4 -- bounded samples (a few probes,
+reduced M), extrapolated linearly in probes x steps and labelled so.  Not the
+headline bench (bench.py measures C3); used for DESIGN.md and profiles/.
 """
 
 import argparse
@@ -19,11 +24,63 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
+def cpu_baseline(name, cfg, op, iv, nnz, gpu_seconds, target_s):
+    """Bounded CPU sample of the config's hot path on this box, extrapolated to the full config."""
+    import numpy as np
+
+    import bench as B
+    from oracle import c_oracle as C
+    from oracle import specdens_oracle as O
+
+    threads = B.cpu_threads()
+    base = {"cores": threads, "cpu_model": B.cpu_model(), "kind": "port", "extrapolated": True}
+    if cfg.method == "lanczos":
+        # lanczos_dos(A, iv, 100, source, n_vec, sigma, grid) of the NumPy/SciPy restatement
+        # (lanczos.py:198-219); OpenBLAS threading left at its default
+        import paper_1308_5467_b200 as sdb
+
+        grid = sdb.interval_grid(iv, cfg.grid_points)
+        sample = 2
+        t0 = time.perf_counter()
+        O.lanczos_dos(op.csr, cfg.degree, cfg.probe_kind, 0, sample, cfg.sigma, grid)
+        secs = time.perf_counter() - t0
+        full = secs * cfg.n_vec / sample
+        return dict(base, seconds_full_config_extrapolated=full, gpu_speedup=full / gpu_seconds,
+                    sample=f"{name}: lanczos_dos with {sample} of {cfg.n_vec} probes, m={cfg.degree} steps, full "
+                           f"reorthogonalisation (oracle/specdens_oracle.py, NumPy/SciPy, default BLAS threads): "
+                           f"{secs:.2f} s; time ~ probes")
+    if hasattr(op, "offsets"):  # stencil operator (C5, C2 as generated): the C oracle's stencil path
+        probes = min(cfg.n_vec, threads)
+        pr = np.array([O.draw_probe(cfg.probe_kind, 0, op.dim, l) for l in range(probes)])
+
+        def run(deg):
+            t0 = time.perf_counter()
+            C.stencil_moments(op, iv.center, iv.halfwidth, deg, pr, mode="doubling", threads=threads)
+            return time.perf_counter() - t0
+
+        cal = run(4)
+        deg = max(4, min(cfg.degree, int(target_s / (cal / 4)) // 2 * 2))
+        secs = run(deg)
+        rate = nnz * probes * deg / secs / 1e9
+    else:
+        sm = B.CpuSampler(op, iv, cfg, True, 0, target_s)
+        secs = sm.sample()
+        probes, deg, rate = sm.probes, sm.degree, sm.rate(secs)
+    full = nnz * cfg.n_vec * cfg.degree / rate / 1e9
+    return dict(base, value=rate, unit="GNNZ-vec/s", cores=min(threads, probes),
+                seconds_full_config_extrapolated=full, gpu_speedup=full / gpu_seconds,
+                sample=f"{name}: {probes} of {cfg.n_vec} probes x M={deg} of {cfg.degree} (doubling), C restatement "
+                       f"of the reference recurrence (oracle/c), one probe per pthread: {secs:.2f} s; rate of the "
+                       "truncated run = extrapolated full-config rate (time ~ steps x probes)")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--format", default="native", choices=["native", "csr", "csr-raw"])
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--cpu", action="store_true", help="time the CPU oracle beside each config (bounded sample)")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="target wall time of one CPU sample")
     args = ap.parse_args()
     if args.format == "csr-raw":
         os.environ["SDB_AUTO_STENCIL"] = "0"
@@ -115,6 +172,11 @@ def main():
                    "achieved_GBs": bytes_launch / (k / steps) / 1e9,
                    "frac_of_peak": bytes_launch / (k / steps) / 1e9 / peak, "nonfinite": bool(nonfinite),
                    "gen_s": gen_s}
+        if args.cpu:
+            try:
+                out["cpu_baseline"] = cpu_baseline(name, cfg, op, iv, nnz, out["seconds"], args.cpu_seconds)
+            except Exception as exc:  # the baseline must not sink the GPU line
+                out["cpu_baseline"] = {"failed": repr(exc)}
         print(json.dumps(out), flush=True)
         del op, probes
         E.Workspace.release()
