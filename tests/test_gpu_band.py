@@ -156,3 +156,65 @@ def test_band_kernel_small_band_and_tail_tile():
         ref = c_oracle.cheb_moments(mat.csr, iv.center, iv.halfwidth, 50, np.array([src.draw(l) for l in range(16)]),
                                     mode=mode, threads=4)
         assert rel(z, ref) <= 1e-10
+
+
+def _banded(n, half_band, n_pairs, seed, heavy_row=None):
+    """Dense-band symmetric matrix plus random far pairs (optionally one row with many)."""
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    for d in range(half_band + 1):
+        v = rng.standard_normal(n - d)
+        i = np.arange(n - d)
+        rows += [i, i + d] if d else [i]
+        cols += [i + d, i] if d else [i]
+        vals += [v, v] if d else [v]
+    i = rng.integers(0, n, n_pairs)
+    j = rng.integers(0, n, n_pairs)
+    if heavy_row is not None:
+        j2 = np.setdiff1d(np.arange(n), np.arange(heavy_row - half_band - 2, heavy_row + half_band + 3))[::3]
+        i = np.concatenate([i, np.full(j2.size, heavy_row)])
+        j = np.concatenate([j, j2])
+    keep = np.abs(i - j) > half_band + 1
+    i, j = i[keep], j[keep]
+    key = np.unique(np.minimum(i, j) * n + np.maximum(i, j))
+    i, j = key // n, key % n
+    v = rng.standard_normal(i.size)
+    rows += [i, j]
+    cols += [j, i]
+    vals += [v, v]
+    a = sp.coo_array((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))), shape=(n, n)).tocsr()
+    a.sort_indices()
+    return sdb.SparseSymmetricMatrix(csr=a)
+
+
+@pytest.mark.parametrize("half_band,kernel_hb", [(6, 8), (13, 16), (22, 24), (30, 32)])
+def test_every_band_half_width_instantiation(half_band, kernel_hb):
+    """One kernel instantiation per supported half-width (the detected band is
+    rounded up); 24 and 32 run the shallower gather ring."""
+    n = 1500
+    mat = _banded(n, half_band, 6 * n, seed=half_band)
+    iv = W.gershgorin_interval(mat)
+    dm, name = kernel_of(mat, 20, _native.SDB_CHEB_DOUBLING)
+    assert dm.band_half_width == kernel_hb and name == "cheb_step_band"
+    src = sdb.ProbeVectorSource("gaussian", seed=9, dim=n)
+    probes = np.array([src.draw(l) for l in range(20)])
+    for mode in ("doubling", "direct"):
+        z = moments(mat, iv, 40, src, 20, MODES[mode])
+        ref = c_oracle.cheb_moments(mat.csr, iv.center, iv.halfwidth, 40, probes, mode=mode, threads=4)
+        assert rel(z, ref) <= 1e-10
+
+
+def test_band_only_and_heavy_far_row():
+    """A matrix with no far entries at all (every stream is four empty batches)
+    and one whose row 700 couples to ~450 far columns (a 100+-batch chunk next
+    to near-empty ones)."""
+    n = 1400
+    for mat in (_banded(n, 10, 0, seed=1), _banded(n, 10, 2 * n, seed=2, heavy_row=700)):
+        iv = W.gershgorin_interval(mat)
+        dm, name = kernel_of(mat, 16, _native.SDB_CHEB_DOUBLING)
+        assert name == "cheb_step_band"
+        src = sdb.ProbeVectorSource("rademacher", seed=3, dim=n)
+        probes = np.array([src.draw(l) for l in range(16)])
+        z = moments(mat, iv, 60, src, 16, MODES["doubling"])
+        ref = c_oracle.cheb_moments(mat.csr, iv.center, iv.halfwidth, 60, probes, mode="doubling", threads=4)
+        assert rel(z, ref) <= 1e-10
