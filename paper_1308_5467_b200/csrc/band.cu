@@ -47,6 +47,8 @@
 #include <cub/cub.cuh>
 
 #include <cstdlib>
+#include <mutex>
+#include <type_traits>
 #include <vector>
 
 #include "stepargs.cuh"
@@ -141,6 +143,7 @@ struct BandArgs {
   int slotA, slotB, slot0;
   int legendre;
   double la, lb, lc;
+  uint64_t keep_pol, once_pol;  // L2 evict_last / evict_first policies (made once per device, band_policies)
   int diag;             // diagnostics (SDB_BAND_DIAG): 4 skip the band, 8 no stage loads, 16 no far
                         // warps (wrong results; timing only)
 };
@@ -193,7 +196,7 @@ __device__ __forceinline__ void band_far_warp(const BandArgs& a, int w, int lane
   constexpr int kPending = (NB < kRecAhead ? NB : kRecAhead) - 1;
   constexpr int kMask = (kRecRing - 1) * kSlotBytes;
   const int g = lane >> 3, q = lane & 7;
-  const uint64_t keep = policy_evict_last(), once = policy_evict_first();
+  const uint64_t keep = a.keep_pol, once = a.once_pol;
   const int G = gridDim.x;
   const int total = a.nslices * a.ntiles;
   const char* const stop_rec = a.frec + a.stop_rec * kRecBytes + lane * 16;
@@ -244,59 +247,65 @@ __device__ __forceinline__ void band_far_warp(const BandArgs& a, int w, int lane
     request(it);
     cp_async_commit();
   }
-  bool consume = false;
-  for (;;) {
-#pragma unroll
-    for (int bb = 0; bb < NB; ++bb, ++it) {
-      cp_async_wait<kPending>();
-      __syncwarp();
-      // every shared-memory operand of this step is requested up front (the
-      // addresses depend on `it` only), so the step pays one LDS round trip
-      const char* recC = ring + (((it - kRecAhead - NB) << 8) & kMask);
-      const char* recI = ring + (((it - kRecAhead) << 8) & kMask);
+  // one step of the walk; CONSUME is false for the first NB steps (nothing gathered yet)
+  auto step = [&](int bb, auto consume_tag) -> bool {
+    constexpr bool CONSUME = decltype(consume_tag)::value;
+    cp_async_wait<kPending>();
+    __syncwarp();
+    // every shared-memory operand of this step is requested up front (the
+    // addresses depend on `it` only), so the step pays one LDS round trip
+    const char* recC = ring + (((it - kRecAhead - NB) << 8) & kMask);
+    const char* recI = ring + (((it - kRecAhead) << 8) & kMask);
+    const uint32_t flagsI = *reinterpret_cast<const uint32_t*>(recI + kRecMeta);
+    const int4 c4 = *reinterpret_cast<const int4*>(recI + g * 16);
+    if (CONSUME) {
       const uint2 meta = *reinterpret_cast<const uint2*>(recC + kRecMeta);
       const double2 v01 = lds2(recC + kRecVal + g * 32), v23 = lds2(recC + kRecVal + g * 32 + 16);
       const double2 g0 = lds2(mine + (bb * 4 + 0) * 512), g1 = lds2(mine + (bb * 4 + 1) * 512),
                     g2 = lds2(mine + (bb * 4 + 2) * 512), g3 = lds2(mine + (bb * 4 + 3) * 512);
-      const uint32_t flagsI = *reinterpret_cast<const uint32_t*>(recI + kRecMeta);
-      const int4 c4 = *reinterpret_cast<const int4*>(recI + g * 16);
-      if (consume) {
-        acc.x = fma(v01.x, g0.x, acc.x);
-        acc.y = fma(v01.x, g0.y, acc.y);
-        acc.x = fma(v01.y, g1.x, acc.x);
-        acc.y = fma(v01.y, g1.y, acc.y);
-        acc.x = fma(v23.x, g2.x, acc.x);
-        acc.y = fma(v23.x, g2.y, acc.y);
-        acc.x = fma(v23.y, g3.x, acc.x);
-        acc.y = fma(v23.y, g3.y, acc.y);
-        if (meta.x) {  // cold: ~1 step in 5
-          if (meta.x & kRecStop) return;
-          // chunk done: its rows' far sums go to the shared tile
-          const int row = (meta.y >> (8 * g)) & 255;
-          *reinterpret_cast<double2*>(yfar + ((size_t)(seq & 1) * kBandR + row) * kBandS + 2 * q) = acc;
-          acc = make_double2(0.0, 0.0);
-          if (meta.x & kRecTileEnd) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&full[seq & 1]);
-            ++seq;
-            const int use = seq >> 1;  // the next tile's buffer must have been read by the band warps
-            if (use > 0) mbar_wait(&empty[seq & 1], (use - 1) & 1);
-          }
+      acc.x = fma(v01.x, g0.x, acc.x);
+      acc.y = fma(v01.x, g0.y, acc.y);
+      acc.x = fma(v01.y, g1.x, acc.x);
+      acc.y = fma(v01.y, g1.y, acc.y);
+      acc.x = fma(v23.x, g2.x, acc.x);
+      acc.y = fma(v23.x, g2.y, acc.y);
+      acc.x = fma(v23.y, g3.x, acc.x);
+      acc.y = fma(v23.y, g3.y, acc.y);
+      if (meta.x) {  // cold: ~1 step in 5
+        if (meta.x & kRecStop) return false;
+        // chunk done: its rows' far sums go to the shared tile
+        const int row = (meta.y >> (8 * g)) & 255;
+        *reinterpret_cast<double2*>(yfar + ((size_t)(seq & 1) * kBandR + row) * kBandS + 2 * q) = acc;
+        acc = make_double2(0.0, 0.0);
+        if (meta.x & kRecTileEnd) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&full[seq & 1]);
+          ++seq;
+          const int use = seq >> 1;  // the next tile's buffer must have been read by the band warps
+          if (use > 0) mbar_wait(&empty[seq & 1], (use - 1) & 1);
         }
       }
-      request(it);
-      if (c4.x >= 0) cp_async16(mine + (bb * 4 + 0) * 512, xrow + (int64_t)(uint32_t)c4.x * kBandS, keep);
-      if (c4.y >= 0) cp_async16(mine + (bb * 4 + 1) * 512, xrow + (int64_t)(uint32_t)c4.y * kBandS, keep);
-      if (c4.z >= 0) cp_async16(mine + (bb * 4 + 2) * 512, xrow + (int64_t)(uint32_t)c4.z * kBandS, keep);
-      if (c4.w >= 0) cp_async16(mine + (bb * 4 + 3) * 512, xrow + (int64_t)(uint32_t)c4.w * kBandS, keep);
-      cp_async_commit();
-      if (flagsI & kRecTileEnd) {  // cold: the next issued record belongs to the block's next tile
-        is_item += G;
-        if (is_item < total)
-          xrow = a.x + (int64_t)(is_item / a.ntiles) * a.sstride + (int64_t)P * kBandS + 2 * q;
-      }
     }
-    consume = true;
+    request(it);
+    if (c4.x >= 0) cp_async16(mine + (bb * 4 + 0) * 512, xrow + (int64_t)(uint32_t)c4.x * kBandS, keep);
+    if (c4.y >= 0) cp_async16(mine + (bb * 4 + 1) * 512, xrow + (int64_t)(uint32_t)c4.y * kBandS, keep);
+    if (c4.z >= 0) cp_async16(mine + (bb * 4 + 2) * 512, xrow + (int64_t)(uint32_t)c4.z * kBandS, keep);
+    if (c4.w >= 0) cp_async16(mine + (bb * 4 + 3) * 512, xrow + (int64_t)(uint32_t)c4.w * kBandS, keep);
+    cp_async_commit();
+    if (flagsI & kRecTileEnd) {  // cold: the next issued record belongs to the block's next tile
+      is_item += G;
+      if (is_item < total)
+        xrow = a.x + (int64_t)(is_item / a.ntiles) * a.sstride + (int64_t)P * kBandS + 2 * q;
+    }
+    ++it;
+    return true;
+  };
+#pragma unroll
+  for (int bb = 0; bb < NB; ++bb) step(bb, std::false_type{});
+  for (;;) {
+#pragma unroll
+    for (int bb = 0; bb < NB; ++bb)
+      if (!step(bb, std::true_type{})) return;
   }
 }
 
@@ -347,7 +356,7 @@ __device__ __forceinline__ void band_band_warps(const BandArgs& a, int tb, char*
   constexpr int P = L::P, R = kBandR, RT = kBandRT, S = kBandS, XW = L::XW, UW = L::UW;
   const int lane = tb & 31, wb = tb >> 5;
   const int g8 = tb >> 3, q = tb & 7, rl = g8 * RT;
-  const uint64_t once = policy_evict_first(), keep = policy_evict_last();
+  const uint64_t once = a.once_pol, keep = a.keep_pol;
   const int G = gridDim.x, b = blockIdx.x;
   const int total = a.nslices * a.ntiles;
   double* red = reinterpret_cast<double*>(smem + L::kRed);
@@ -815,6 +824,34 @@ int band_build(sdb_matrix* m, cudaStream_t s) {
   return SDB_OK;
 }
 
+// The two L2 cache policies as plain 64-bit values: created once per device by a
+// one-thread kernel and passed as kernel arguments, so they reach the copy
+// instructions from the constant bank (uniform registers) instead of being
+// re-materialised per use.
+__global__ void band_policy_kernel(uint64_t* out) {
+  out[0] = policy_evict_last();
+  out[1] = policy_evict_first();
+}
+static int band_policies(int device, uint64_t* keep, uint64_t* once) {
+  static std::mutex mu;
+  static uint64_t cache[64][2];
+  static bool have[64] = {};
+  std::lock_guard<std::mutex> lock(mu);
+  if (device < 0 || device >= 64) return fail(SDB_EINVAL, "device index %d out of range", device);
+  if (!have[device]) {
+    uint64_t* d = nullptr;
+    SDB_CUDA(cudaMalloc(&d, 2 * sizeof(uint64_t)));
+    band_policy_kernel<<<1, 1>>>(d);
+    cudaError_t e = cudaMemcpy(cache[device], d, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return cuda_fail(e, "band policy kernel", __FILE__, __LINE__);
+    have[device] = true;
+  }
+  *keep = cache[device][0];
+  *once = cache[device][1];
+  return SDB_OK;
+}
+
 // ---- host planning / launch ---------------------------------------------------------
 #define SDB_BAND_HB(HBV, CASE) \
   do {                         \
@@ -926,6 +963,7 @@ int band_launch_step(const sdb_matrix* m, const BandPlan& p, const StepArgs& a, 
   ba.lb = a.lb;
   ba.lc = a.lc;
   if (const char* e = getenv("SDB_BAND_DIAG")) ba.diag = atoi(e);
+  if (int prc = band_policies(m->device, &ba.keep_pol, &ba.once_pol)) return prc;
   const bool shallow = band_shallow_ring();
   int rc = SDB_OK;
 #define SDB_BAND_LAUNCH(HBV)                                         \
