@@ -82,6 +82,7 @@ struct ZmGeom {
   static constexpr int PX = TX + 2, PY = TY + 2;   // halo box extent
   static constexpr int BOX = PY * PX * CS;         // doubles per plane box
   static_assert((TX * TY) % GROUPS == 0, "tile must split evenly over the point groups");
+  static_assert(PPT == 1 || (PPT == 2 && TY % 2 == 0), "columns per thread: 1, or 2 (a y pair)");
   static_assert(NT % 32 == 0 && NT <= 1024 - 32, "consumer threads");
 };
 
@@ -210,8 +211,11 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
     int64_t cofs[PPT];  // padded block offset of (z = zbeg, y, x) + column
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
+      // PPT == 2: the two columns are neighbours in y (rows 2j, 2j+1), so their
+      // 3x3 neighbourhoods share a 4x3 window of loads; a warp's points stay
+      // consecutive in x (conflict-free 16-byte loads for every CS)
       const int pnt = g + k * GROUPS;
-      const int px = pnt % TX, py = pnt / TX;
+      const int px = PPT == 2 ? g % TX : pnt % TX, py = PPT == 2 ? 2 * (g / TX) + k : pnt / TX;
       cx[k] = xt * TX + px;
       cy[k] = yt * TY + py;
       xo[k] = ((py + 1) * (TX + 2) + (px + 1)) * CS + 2 * q;  // centre in the x halo box
@@ -226,31 +230,64 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
     for (int k = 0; k < PPT; ++k) accN[k] = accC[k] = accP[k] = make_double2(0.0, 0.0);
     double* pn = a.next - 2 * pplane;  // output plane p - 1 (+ cofs), for p = zbeg - 1 first
     int sprev = -1;  // slot of plane p - 1 (this item), released after its epilogue
+    double2 xcen[PPT], xcen_prev[PPT];  // x at the columns' own points, planes p and p - 1 (PPT == 2)
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) xcen[k] = xcen_prev[k] = make_double2(0.0, 0.0);
     for (int p = zbeg - 1; p <= zend; ++p) {
       mbar_wait(full + s, phase);
       const double* slot = zsm + (int64_t)s * SL::DOUBLES;
       const bool outp = p >= zbeg && p < zend;
       // plane p: per column, the 3x3 (or star) neighbourhood into registers,
       // then its terms in lexicographic (dz, dy, dx) order
+      if constexpr (PPT == 2) {
+        // rows py0-1 .. py0+2 of the halo box, x-1 .. x+1: 12 loads (27-point) or
+        // 8 (7-point) serve both columns instead of 18 / 10
+        double2 nbw[4][3];
 #pragma unroll
-      for (int k = 0; k < PPT; ++k) {
-        const double dg = outp ? slot[SL::D0 + dio[k]] : 0.0;
-        double2 nb[9];
+        for (int r = 0; r < 4; ++r)
 #pragma unroll
-        for (int e = 0; e < 9; ++e) {
-          if (!((PMASK >> e) & 1)) continue;
-          const int dy = e / 3 - 1, dx = e % 3 - 1;
-          nb[e] = *reinterpret_cast<const double2*>(slot + SL::X0 + xo[k] + (dy * (TX + 2) + dx) * CS);
+          for (int c = 0; c < 3; ++c) {
+            const bool need = (r <= 2 && ((PMASK >> (r * 3 + c)) & 1)) || (r >= 1 && ((PMASK >> ((r - 1) * 3 + c)) & 1));
+            if (need)
+              nbw[r][c] =
+                  *reinterpret_cast<const double2*>(slot + SL::X0 + xo[0] + ((r - 1) * (TX + 2) + (c - 1)) * CS);
+          }
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) {
+          const double dg = outp ? slot[SL::D0 + dio[k]] : 0.0;
+          xcen_prev[k] = xcen[k];
+          xcen[k] = nbw[1 + k][1];
+#pragma unroll
+          for (int o = 0; o < G::NT; ++o) {
+            const double2 v = nbw[G::dy(o) + 1 + k][G::dx(o) + 1];
+            const bool centre = G::dx(o) == 0 && G::dy(o) == 0 && G::dz(o) == 0;
+            const double w = centre ? dg : t.wc[o];
+            double2& y = G::dz(o) < 0 ? accN[k] : (G::dz(o) == 0 ? accC[k] : accP[k]);
+            y.x = fma(w, v.x, y.x);
+            y.y = fma(w, v.y, y.y);
+          }
         }
+      } else {
 #pragma unroll
-        for (int o = 0; o < G::NT; ++o) {
-          const int e = (G::dy(o) + 1) * 3 + G::dx(o) + 1;
-          const double2 v = nb[e];
-          const bool centre = G::dx(o) == 0 && G::dy(o) == 0 && G::dz(o) == 0;
-          const double w = centre ? dg : t.wc[o];
-          double2& y = G::dz(o) < 0 ? accN[k] : (G::dz(o) == 0 ? accC[k] : accP[k]);
-          y.x = fma(w, v.x, y.x);
-          y.y = fma(w, v.y, y.y);
+        for (int k = 0; k < PPT; ++k) {
+          const double dg = outp ? slot[SL::D0 + dio[k]] : 0.0;
+          double2 nb[9];
+#pragma unroll
+          for (int e = 0; e < 9; ++e) {
+            if (!((PMASK >> e) & 1)) continue;
+            const int dy = e / 3 - 1, dx = e % 3 - 1;
+            nb[e] = *reinterpret_cast<const double2*>(slot + SL::X0 + xo[k] + (dy * (TX + 2) + dx) * CS);
+          }
+#pragma unroll
+          for (int o = 0; o < G::NT; ++o) {
+            const int e = (G::dy(o) + 1) * 3 + G::dx(o) + 1;
+            const double2 v = nb[e];
+            const bool centre = G::dx(o) == 0 && G::dy(o) == 0 && G::dz(o) == 0;
+            const double w = centre ? dg : t.wc[o];
+            double2& y = G::dz(o) < 0 ? accN[k] : (G::dz(o) == 0 ? accC[k] : accP[k]);
+            y.x = fma(w, v.x, y.x);
+            y.y = fma(w, v.y, y.y);
+          }
         }
       }
       // out(p-1) is complete: its operands are in the previous slot
@@ -258,7 +295,7 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
         const double* ps = zsm + (int64_t)sprev * SL::DOUBLES;
 #pragma unroll
         for (int k = 0; k < PPT; ++k) {
-          const double2 xi = *reinterpret_cast<const double2*>(ps + SL::X0 + xo[k]);
+          const double2 xi = PPT == 2 ? xcen_prev[k] : *reinterpret_cast<const double2*>(ps + SL::X0 + xo[k]);
           const double tx = (accP[k].x - a.c * xi.x) * a.inv_d;
           const double ty = (accP[k].y - a.c * xi.y) * a.inv_d;
           double2 wn;
