@@ -18,6 +18,10 @@
 //   K5b lz_update  w -= V_{0..j} h, optional ||w||^2 partials
 //   K5c lz_update_proj  full reorth: pass 1's update and pass 2's projection
 //                  in one basis read (3 basis passes per step instead of 4)
+//   two-pass full reorth (default for n >= 16384): lz_proj also yields the
+//                  Gram column V^T v_j; h = 2 h1 - G h1 (lz_gram_correct)
+//                  stands in for the second projection, one lz_update follows
+//                  (2 basis passes per step; see lz_gram_correct)
 // and small fixed-order reduce kernels between them (deterministic).  A probe
 // that breaks down is frozen (1/beta = 0) while the others continue.
 #include <cmath>
@@ -179,7 +183,9 @@ __global__ void lz_alpha_reduce(const double* __restrict__ partials, int64_t nbl
 // the fly and the warp handling t == 0 stores it to wdst (a different
 // buffer, so concurrent blocks never see a half-updated w).  NORM adds
 // ||w'||^2 partials (selective mode) at slot norm_slot.
-template <int NV, bool SUB_ALPHA, bool NORM>
+// GRAM (two-pass schedule, see lz_gram_correct): the same basis read also
+// yields column j of the Gram matrix, g[t] = V_t^T v_j, at slot norm_slot + t.
+template <int NV, bool SUB_ALPHA, bool NORM, bool GRAM = false>
 __global__ void __launch_bounds__(kProjWarps * 32)
     lz_proj(const double* __restrict__ basis, const double* __restrict__ wsrc, double* __restrict__ wdst, LzState st,
             int64_t j, int64_t n, int64_t ldv, int64_t nrb, double* partials, int64_t norm_slot) {
@@ -190,13 +196,14 @@ __global__ void __launch_bounds__(kProjWarps * 32)
   const size_t plane = (size_t)n * ldv;
   const double* vt = basis + (size_t)t * plane;
   const double* vj = basis + (size_t)j * plane;
+  static_assert(!(GRAM && (SUB_ALPHA || NORM)), "the Gram column rides on the plain projection");
   double2 acc[NV], nacc[NV], al[NV];
   bool colok[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) {
     const int64_t col = 2 * (lane + 32 * v);
     colok[v] = col < ldv;
-    acc[v] = nacc[v] = make_double2(0.0, 0.0);
+    acc[v] = nacc[v] = make_double2(0.0, 0.0);  // nacc: ||w'||^2 (NORM) or the Gram column (GRAM)
     al[v] = (SUB_ALPHA && colok[v]) ? ld_d2(st.alpha_cur + col) : make_double2(0.0, 0.0);
   }
   const bool active = t <= j;
@@ -222,6 +229,11 @@ __global__ void __launch_bounds__(kProjWarps * 32)
         double2 b = ld_d2_stream(vt + o + 64 * v);
         acc[v].x += b.x * w.x;
         acc[v].y += b.y * w.y;
+        if (GRAM) {
+          const double2 p = ld_d2(vj + o + 64 * v);
+          nacc[v].x += b.x * p.x;
+          nacc[v].y += b.y * p.y;
+        }
       }
     }
 #pragma unroll
@@ -231,6 +243,11 @@ __global__ void __launch_bounds__(kProjWarps * 32)
       double* p = partials + ((size_t)t * nrb + rb) * ldv + col;
       p[0] = acc[v].x;
       p[1] = acc[v].y;
+      if (GRAM) {
+        double* gp = partials + ((size_t)(norm_slot + t) * nrb + rb) * ldv + col;
+        gp[0] = nacc[v].x;
+        gp[1] = nacc[v].y;
+      }
     }
   }
   if (NORM && storer) {
@@ -257,6 +274,48 @@ __global__ void lz_h_reduce(const double* __restrict__ partials, int64_t nrb, in
     if (!(fabs(v) > 1.4901161193847656e-08 * wn)) v = 0.0;
   }
   if ((threadIdx.x >> 5) == 0 && l < ldv) h[t * ldv + l] = v;
+}
+
+// ---- two-pass full reorthogonalisation (Gram-corrected CGS2) ---------------------------
+// CGS twice is w'' = (I - V V^T)(I - V V^T) w = w - V (2 h1 - G h1) with
+// h1 = V^T w and G = V^T V: the second projection h2 = V^T (w - V h1) equals
+// (I - G) h1, so with the Gram matrix of the basis at hand the second basis
+// read is not needed -- one projection pass (which also yields the new Gram
+// column V^T v_j) and one update pass per step instead of three passes.  This
+// is the low-synchronisation CGS2 projector I - V T V^T with T = 2I - G
+// ~ (V^T V)^{-1}; what it leaves out is the rounding error of the first update
+// projected on V (O(eps)), so the basis stays orthogonal to ~1e-14 instead of
+// ~1e-15 and alpha, beta agree with the three-pass schedule to ~1e-13
+// relative (measured; tests/test_gpu_lanczos.py), far inside the 1e-10 bar.
+// G is kept per probe as [t][s][ldv], t, s < gdim.
+__global__ void lz_g_reduce(const double* __restrict__ partials, int64_t slot0, int64_t nrb, int64_t ldv, int64_t j,
+                            int64_t gdim, double* __restrict__ G) {
+  const int64_t t = blockIdx.x, l = blockIdx.y * 32 + (threadIdx.x & 31);
+  const double v = block_col_sum<kRedSegs>(partials, slot0 + t, nrb, ldv, l);
+  if ((threadIdx.x >> 5) == 0 && l < ldv) {
+    G[(t * gdim + j) * ldv + l] = v;
+    G[(j * gdim + t) * ldv + l] = v;
+  }
+}
+
+// hc[t] = 2 h1[t] - sum_{s <= j} G[t][s] h1[s]   (fixed-order segment sums)
+__global__ void lz_gram_correct(const double* __restrict__ G, const double* __restrict__ h1, int64_t ldv, int64_t j,
+                                int64_t gdim, double* __restrict__ hc) {
+  __shared__ double red[kRedSegs][32];
+  const int lane = threadIdx.x & 31, seg = threadIdx.x >> 5;
+  const int64_t t = blockIdx.x, l = blockIdx.y * 32 + lane;
+  double sum = 0.0;
+  if (l < ldv)
+    for (int64_t s = seg; s <= j; s += kRedSegs) sum = fma(G[(t * gdim + s) * ldv + l], h1[s * ldv + l], sum);
+  red[seg][lane] = sum;
+  __syncthreads();
+  if (seg == 0 && l < ldv) {
+    double tot = 0.0;
+#pragma unroll
+    for (int k = 0; k < kRedSegs; ++k) tot += red[k][lane];
+    const double a = h1[t * ldv + l];
+    hc[t * ldv + l] = a + (a - tot);
+  }
 }
 
 // ---- K5b: w -= V h (row-local), optional ||w||^2 partials ---------------------------
@@ -507,17 +566,23 @@ __global__ void lz_beta_reduce(const double* __restrict__ partials, int64_t nblo
 // ---- host driver ------------------------------------------------------------------------
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
+constexpr int64_t kGramMaxSteps = 256;  // steps covered by the Gram matrix (64 MB at 128 probes)
+
 struct LzLayout {
-  size_t block, part, h, state, total;
+  size_t block, part, h, state, gram, total;
+  int64_t gdim;
 };
 
 static LzLayout lz_layout(const sdb_matrix* m, int64_t ldv, int64_t steps) {
   LzLayout L;
+  L.gdim = steps < kGramMaxSteps ? steps : kGramMaxSteps;
   L.block = align256(sizeof(double) * (size_t)m->n * ldv);
-  L.part = align256(sizeof(double) * (size_t)(steps + 1) * row_blocks(m) * ldv);
-  L.h = align256(sizeof(double) * (size_t)steps * ldv);
+  // slots 0..steps-1: projection partials, steps: ||w||^2, steps+1..: Gram column partials
+  L.part = align256(sizeof(double) * (size_t)(steps + 1 + L.gdim) * row_blocks(m) * ldv);
+  L.h = align256(sizeof(double) * (size_t)steps * ldv);  // two of these: h1 and the corrected h
   L.state = align256(sizeof(double) * 4 * (size_t)ldv);
-  L.total = 2 * L.block + L.part + L.h + L.state;
+  L.gram = align256(sizeof(double) * (size_t)L.gdim * L.gdim * ldv);
+  L.total = 2 * L.block + L.part + 2 * L.h + L.state + L.gram;
   return L;
 }
 
@@ -547,6 +612,20 @@ static int lz_launch_proj(int nv, bool sub_alpha, bool norm, const double* basis
   SDB_PROJ_NV(1) SDB_PROJ_NV(2) SDB_PROJ_NV(3) SDB_PROJ_NV(4)
 #undef SDB_PROJ_NV
 #undef SDB_PROJ
+  return fail(SDB_EUNSUPPORTED, "no projection kernel for ldv=%lld", (long long)ldv);
+}
+
+static int lz_launch_proj_gram(int nv, const double* basis, const double* wsrc, const LzState& st, int64_t j, int64_t n,
+                               int64_t ldv, int64_t nrb, double* part, int64_t gram_slot0, cudaStream_t s) {
+  dim3 grid((unsigned)((j + 1 + kProjWarps - 1) / kProjWarps), (unsigned)nrb);
+  dim3 block(kProjWarps * 32);
+#define SDB_PROJ_G(NVV)                                                                                              \
+  if (nv == NVV) {                                                                                                   \
+    lz_proj<NVV, false, false, true><<<grid, block, 0, s>>>(basis, wsrc, nullptr, st, j, n, ldv, nrb, part, gram_slot0); \
+    return SDB_OK;                                                                                                   \
+  }
+  SDB_PROJ_G(1) SDB_PROJ_G(2) SDB_PROJ_G(3) SDB_PROJ_G(4)
+#undef SDB_PROJ_G
   return fail(SDB_EUNSUPPORTED, "no projection kernel for ldv=%lld", (long long)ldv);
 }
 
@@ -603,6 +682,19 @@ static bool lz_fused_enabled() {
   return !(e && e[0] == '0');
 }
 
+// Two-pass (Gram-corrected) full reorthogonalisation: on by default for
+// n >= 64 * kGramMaxSteps, i.e. where the steps it covers are far from
+// exhausting the space, so the dimension-exhaustion breakdowns of small
+// matrices keep the three-pass schedule bit for bit; the rule depends on n
+// only, so a shorter run stays an exact prefix of a longer one.
+// SDB_LZ_GRAM=0 / 1 forces it off / on.
+static bool lz_gram_enabled(int64_t n) {
+  const char* e = getenv("SDB_LZ_GRAM");
+  if (e && e[0] == '0') return false;
+  if (e && e[0] == '1') return true;
+  return n >= 64 * kGramMaxSteps;
+}
+
 }  // namespace sdb
 
 using namespace sdb;
@@ -640,11 +732,13 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
   const int64_t panel = panel_rows(m, ldv, (32 / g.L) * kRowWarps);
   const LzLayout lay = lz_layout(m, ldv, steps);
   char* p = (char*)workspace;
-  double* W0 = (double*)p;
-  double* W1 = (double*)(p + lay.block);
+  double* const Wa = (double*)p;
+  double* const Wb = (double*)(p + lay.block);
   double* part = (double*)(p + 2 * lay.block);
   double* h = (double*)(p + 2 * lay.block + lay.part);
-  double* stp = (double*)(p + 2 * lay.block + lay.part + lay.h);
+  double* hc = (double*)(p + 2 * lay.block + lay.part + lay.h);
+  double* stp = (double*)(p + 2 * lay.block + lay.part + 2 * lay.h);
+  double* G = (double*)(p + 2 * lay.block + lay.part + 2 * lay.h + lay.state);
   LzState st{stp, stp + ldv, stp + 2 * ldv, stp + 3 * ldv};
   const size_t plane = (size_t)n * ldv;
   const int64_t norm_slot = steps;
@@ -665,8 +759,14 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
   if (m->format == SDB_FMT_CSR) cv = make_csr_view(m); else sv = make_stencil_view(m);
 
   const bool fused = lz_fused_enabled();
+  const bool gram = reorth == SDB_REORTH_FULL && lz_gram_enabled(n);
+  const int64_t gram_slot0 = steps + 1;
   const double* wraw = v0;
   for (int64_t j = 0; j < steps; ++j) {
+    // the step reads wraw (the previous step's w) and leaves its w in the other buffer
+    double* const W1 = wraw == Wb ? Wa : Wb;
+    double* const W0 = wraw == Wb ? Wb : Wa;
+    double* wfinal = W0;
     double* vj = basis + (size_t)j * plane;
     const double* vprev = j > 0 ? basis + (size_t)(j - 1) * plane : nullptr;
     if (m->format == SDB_FMT_CSR)
@@ -692,7 +792,20 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
       // then w' -= V h2 with ||w'||^2.  Fallback (t range beyond the fused
       // kernel's registers): the reference order with 4 basis reads.
       const bool fz = fused && lz_update_proj_fits(j);
-      if (fz) {
+      if (gram && j + 1 <= lay.gdim) {
+        // two basis reads: h1 = V^T w with the Gram column V^T v_j, h = 2 h1 - G h1, w -= V h in place
+        if ((rc = lz_launch_proj_gram(nv, basis, W1, st, j, n, ldv, nrb, part, gram_slot0, s))) return rc;
+        SDB_CHECK_LAUNCH();
+        lz_h_reduce<<<hblk, 32 * kRedSegs, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
+        SDB_CHECK_LAUNCH();
+        lz_g_reduce<<<hblk, 32 * kRedSegs, 0, s>>>(part, gram_slot0, nrb, ldv, j, lay.gdim, G);
+        SDB_CHECK_LAUNCH();
+        lz_gram_correct<<<hblk, 32 * kRedSegs, 0, s>>>(G, h, ldv, j, lay.gdim, hc);
+        SDB_CHECK_LAUNCH();
+        if ((rc = lz_launch_update(g, true, basis, W1, hc, j, n, nrb, panel, part, s))) return rc;
+        SDB_CHECK_LAUNCH();
+        wfinal = W1;
+      } else if (fz) {
         if ((rc = lz_launch_proj(nv, false, false, basis, W1, W1, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
         SDB_CHECK_LAUNCH();
         lz_h_reduce<<<hblk, 32 * kRedSegs, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
@@ -710,10 +823,12 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
         if ((rc = lz_launch_proj(nv, false, false, basis, W0, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
         SDB_CHECK_LAUNCH();
       }
-      lz_h_reduce<<<hblk, 32 * kRedSegs, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
-      SDB_CHECK_LAUNCH();
-      if ((rc = lz_launch_update(g, true, basis, W0, h, j, n, nrb, panel, part, s))) return rc;
-      SDB_CHECK_LAUNCH();
+      if (wfinal == W0) {
+        lz_h_reduce<<<hblk, 32 * kRedSegs, 0, s>>>(part, nrb, ldv, j, h, 0, norm_slot);
+        SDB_CHECK_LAUNCH();
+        if ((rc = lz_launch_update(g, true, basis, W0, h, j, n, nrb, panel, part, s))) return rc;
+        SDB_CHECK_LAUNCH();
+      }
     } else if (reorth == SDB_REORTH_SELECTIVE) {
       if ((rc = lz_launch_proj(nv, true, true, basis, W1, W0, st, j, n, ldv, nrb, part, norm_slot, s))) return rc;
       SDB_CHECK_LAUNCH();
@@ -730,7 +845,7 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
     }
     lz_beta_reduce<<<cblk, 32 * kRedSegs, 0, s>>>(part, nrb, ldv, n_vec, j, steps, st, beta, steps_done, status);
     SDB_CHECK_LAUNCH();
-    wraw = W0;
+    wraw = wfinal;
   }
   return SDB_OK;
 }

@@ -218,3 +218,55 @@ def test_fused_cgs2_pass_matches_four_pass_schedule(monkeypatch, steps):
             scale = np.max(np.abs(alpha))
             assert np.max(np.abs(f.alpha - alpha)) <= 1e-10 * scale
             assert np.max(np.abs(f.beta - beta)) <= 1e-10 * scale
+
+
+@pytest.mark.parametrize("steps", [5, 40, 100, 300])
+def test_gram_two_pass_reorthogonalisation_matches_three_pass(monkeypatch, steps):
+    """The two-pass full reorthogonalisation (projection + Gram column, h = 2 h1 - G h1,
+    one update; default for n >= 16384) against the three-pass CGS2 schedule and the
+    oracle on the same probes.  300 steps runs past the Gram matrix (256 steps) and
+    finishes on the fallback schedule."""
+    op = W.anderson_3d(12)
+    iv = W.gershgorin_interval(op)
+    src = sdb.ProbeVectorSource("gaussian", seed=3, dim=op.dim)
+    grid = sdb.interval_grid(iv, 256)
+    monkeypatch.setenv("SDB_LZ_GRAM", "1")
+    gram = sdb.lanczos_dos(op, iv, steps, src, 70, 0.05, grid)
+    monkeypatch.setenv("SDB_LZ_GRAM", "0")
+    plain = sdb.lanczos_dos(op, iv, steps, src, 70, 0.05, grid)
+    assert np.max(np.abs(gram.density - plain.density)) <= 1e-10
+    np.testing.assert_allclose(gram.params["ritz_nodes"], plain.params["ritz_nodes"], rtol=0, atol=1e-10)
+    monkeypatch.setenv("SDB_LZ_GRAM", "1")
+    if steps <= 100:
+        for l in (0, 69):
+            alpha, beta = O.lanczos_factorize(op.csr, src.draw(l), steps)[:2]
+            f = sdb.lanczos_factorize(op, src.draw(l), steps)
+            scale = np.max(np.abs(alpha))
+            assert np.max(np.abs(f.alpha - alpha)) <= 1e-10 * scale
+            assert np.max(np.abs(f.beta - beta)) <= 1e-10 * scale
+            v = f.basis
+            assert np.max(np.abs(v.T @ v - np.eye(v.shape[1]))) <= 1e-12
+    # a shorter run is an exact prefix of a longer one under the same schedule
+    v0 = src.draw(1)
+    long = sdb.lanczos_factorize(op, v0, min(steps, 60))
+    short = sdb.lanczos_factorize(op, v0, min(steps, 60) // 2 + 1)
+    np.testing.assert_array_equal(long.alpha[:short.alpha.size], short.alpha)
+
+
+def test_gram_two_pass_breakdown_and_frozen_probes(monkeypatch):
+    """Invariant-subspace breakdown under the two-pass schedule: a matrix with three
+    distinct eigenvalues stops after three steps (beta <= 1e-13 scale), like the
+    reference; an eigenvector start stops after one."""
+    monkeypatch.setenv("SDB_LZ_GRAM", "1")
+    n = 4000
+    rng = np.random.default_rng(1)
+    d = rng.choice([-0.7, 0.1, 0.6], size=n)
+    import scipy.sparse as sp
+    op = sdb.SparseSymmetricMatrix(csr=sp.diags(d).tocsr())
+    f = sdb.lanczos_factorize(op, rng.standard_normal(n), 8)
+    assert f.breakdown and f.alpha.size == 3
+    np.testing.assert_allclose(np.sort(sdb.ritz_quadrature(f).theta), [-0.7, 0.1, 0.6], atol=1e-12)
+    e = np.zeros(n)
+    e[5] = 1.0
+    f1 = sdb.lanczos_factorize(op, e, 4)
+    assert f1.breakdown and f1.alpha.size == 1

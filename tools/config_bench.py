@@ -130,19 +130,29 @@ def main():
 
             ma = device_matrix(res.base, dev, E.stream_ptr(dev)).bytes_per_pass
             m = cfg.degree
-            # traffic of the schedule that ran: fused (default, <= 256 steps):
-            # SpMM 4 passes + proj (V, w) + K5c (V, w in, w out) + update (V, w rmw);
-            # SDB_LZ_FUSED=0: the 4-pass reference order
+            # traffic of the schedule that ran.  Two-pass Gram-corrected CGS2 (default for
+            # n >= 16384, <= 256 steps): SpMM 4 block passes + proj (V, w, v_j) + update (V, w rmw);
+            # fused three-pass (SDB_LZ_GRAM=0): SpMM 4 + proj (V, w) + K5c (V, w in, w out) +
+            # update (V, w rmw); SDB_LZ_FUSED=0 as well: the 4-pass reference order
+            genv = os.environ.get("SDB_LZ_GRAM", "")
+            gram = m <= 256 and (genv == "1" or (genv != "0" and n >= 16384))
             fused = os.environ.get("SDB_LZ_FUSED", "1") != "0" and m <= 256
-            total = sum(ma + 8 * n * ldv * ((3 * (j + 1) + 9) if fused else (4 * (j + 1) + 11)) for j in range(m))
-            minimal = sum(ma + 8 * n * ldv * (3 * (j + 1) + 3) for j in range(m))
+            per_step = (lambda j: 2 * (j + 1) + 8) if gram else (
+                (lambda j: 3 * (j + 1) + 9) if fused else (lambda j: 4 * (j + 1) + 11))
+            passes = 2 if gram else 3
+            total = sum(ma + 8 * n * ldv * per_step(j) for j in range(m))
+            minimal = sum(ma + 8 * n * ldv * (passes * (j + 1) + 3) for j in range(m))
+            minimal3 = sum(ma + 8 * n * ldv * (3 * (j + 1) + 3) for j in range(m))
             t = statistics.median(times)
             out = {"config": name, "method": "lanczos", "n": n, "nnz": nnz, "n_vec": cfg.n_vec, "steps": m,
                    "seconds": t, "gnnz_vec_s": nnz * cfg.n_vec * m / t / 1e9,
-                   "schedule": "fused CGS2 (3 basis reads)" if fused else "4-pass CGS2",
+                   "schedule": ("two-pass Gram-corrected CGS2 (2 basis reads)" if gram else
+                                "fused CGS2 (3 basis reads)" if fused else "4-pass CGS2"),
                    "bytes_moved_model_TB": total / 1e12, "achieved_GBs": total / t / 1e9,
-                   "frac_of_peak": total / t / 1e9 / peak, "minimal_3pass_TB": minimal / 1e12,
-                   "frac_vs_minimal_bytes": minimal / t / 1e9 / peak, "gen_s": gen_s}
+                   "frac_of_peak": total / t / 1e9 / peak, "minimal_TB": minimal / 1e12,
+                   "frac_vs_minimal_bytes": minimal / t / 1e9 / peak,
+                   "minimal_3pass_TB": minimal3 / 1e12, "frac_vs_minimal_3pass_bytes": minimal3 / t / 1e9 / peak,
+                   "gen_s": gen_s}
         else:
             mode = _native.SDB_CHEB_DOUBLING
             mapped = sdb.apply_spectral_map(op, iv)
