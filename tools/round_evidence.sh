@@ -17,6 +17,11 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 1200 --csv --log-fi
   python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cold > $O/${TAG}_ncu_launch.log 2>&1
 python tools/launch_summary.py $O/${TAG}_launches_c3.csv $O/${TAG}_launches_c3.txt \
   "ncu launch list: python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-cold (C3)" > /dev/null
+# C4 Lanczos launch list (two-pass Gram-corrected reorthogonalisation)
+ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv --log-file $O/${TAG}_launches_c4.csv \
+  python tools/config_bench.py C4 --reps 1 > $O/${TAG}_ncu_launch_c4.log 2>&1
+python tools/launch_summary.py $O/${TAG}_launches_c4.csv $O/${TAG}_launches_c4.txt \
+  "C4 Lanczos (m=100, 128 probes) launch list, config_bench --reps 1" > /dev/null
 # ncu --set full of one band step and one C5 z-march step
 ncu --set full --import-source on --clock-control none -k regex:cheb_step_band -s 3 -c 1 -o $O/${TAG}_band_c3 -f \
   python tools/prof_step.py C3 12 > $O/${TAG}_ncu_band.log 2>&1
