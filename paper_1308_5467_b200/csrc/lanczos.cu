@@ -18,7 +18,7 @@
 //   K5b lz_update  w -= V_{0..j} h, optional ||w||^2 partials
 //   K5c lz_update_proj  full reorth: pass 1's update and pass 2's projection
 //                  in one basis read (3 basis passes per step instead of 4)
-//   two-pass full reorth (default for n >= 16384): lz_proj also yields the
+//   two-pass full reorth (default for n >= 16384, steps <= n / 64): lz_proj also yields the
 //                  Gram column V^T v_j; h = 2 h1 - G h1 (lz_gram_correct)
 //                  stands in for the second projection, one lz_update follows
 //                  (2 basis passes per step; see lz_gram_correct)
@@ -566,7 +566,21 @@ __global__ void lz_beta_reduce(const double* __restrict__ partials, int64_t nblo
 // ---- host driver ------------------------------------------------------------------------
 static size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
 
-constexpr int64_t kGramMaxSteps = 256;  // steps covered by the Gram matrix (64 MB at 128 probes)
+// Two-pass (Gram-corrected) full reorthogonalisation covers steps j < gdim:
+// default gdim = n / 64 for n >= kGramMinRows (the run stays far from
+// exhausting the space, so the dimension-exhaustion breakdowns of small
+// matrices keep the three-pass schedule bit for bit; the rule depends on n and
+// j only, so a shorter run stays an exact prefix of a longer one).  The Gram
+// matrix is gdim^2 x ldv doubles, at most 1/64 of the basis.  SDB_LZ_GRAM=0 /
+// 1 forces the schedule off / on for every step.
+constexpr int64_t kGramMinRows = 16384;
+static int64_t lz_gram_steps(int64_t n, int64_t steps) {
+  const char* e = getenv("SDB_LZ_GRAM");
+  if (e && e[0] == '0') return 0;
+  if (e && e[0] == '1') return steps;
+  if (n < kGramMinRows) return 0;
+  return steps < n / 64 ? steps : n / 64;
+}
 
 struct LzLayout {
   size_t block, part, h, state, gram, total;
@@ -575,7 +589,7 @@ struct LzLayout {
 
 static LzLayout lz_layout(const sdb_matrix* m, int64_t ldv, int64_t steps) {
   LzLayout L;
-  L.gdim = steps < kGramMaxSteps ? steps : kGramMaxSteps;
+  L.gdim = lz_gram_steps(m->n, steps);
   L.block = align256(sizeof(double) * (size_t)m->n * ldv);
   // slots 0..steps-1: projection partials, steps: ||w||^2, steps+1..: Gram column partials
   L.part = align256(sizeof(double) * (size_t)(steps + 1 + L.gdim) * row_blocks(m) * ldv);
@@ -682,19 +696,6 @@ static bool lz_fused_enabled() {
   return !(e && e[0] == '0');
 }
 
-// Two-pass (Gram-corrected) full reorthogonalisation: on by default for
-// n >= 64 * kGramMaxSteps, i.e. where the steps it covers are far from
-// exhausting the space, so the dimension-exhaustion breakdowns of small
-// matrices keep the three-pass schedule bit for bit; the rule depends on n
-// only, so a shorter run stays an exact prefix of a longer one.
-// SDB_LZ_GRAM=0 / 1 forces it off / on.
-static bool lz_gram_enabled(int64_t n) {
-  const char* e = getenv("SDB_LZ_GRAM");
-  if (e && e[0] == '0') return false;
-  if (e && e[0] == '1') return true;
-  return n >= 64 * kGramMaxSteps;
-}
-
 }  // namespace sdb
 
 using namespace sdb;
@@ -759,7 +760,7 @@ int sdb_lanczos(const sdb_matrix* m, double c, double d, int64_t n_vec, int64_t 
   if (m->format == SDB_FMT_CSR) cv = make_csr_view(m); else sv = make_stencil_view(m);
 
   const bool fused = lz_fused_enabled();
-  const bool gram = reorth == SDB_REORTH_FULL && lz_gram_enabled(n);
+  const bool gram = reorth == SDB_REORTH_FULL && lay.gdim > 0;
   const int64_t gram_slot0 = steps + 1;
   const double* wraw = v0;
   for (int64_t j = 0; j < steps; ++j) {

@@ -53,6 +53,7 @@ struct ZmArgs {
   int z_lo, z_hi;             // planes computed: [z_lo, z_hi) (row partition: a slab's planes)
   const double* diag;         // n (unpadded)
   int hint;                   // L2 policies on the TMA loads: 1 = w_{k-1} / v0 boxes evict_first, 2 = x boxes evict_last
+  int order, gtiles, sw;      // item order (zm_decode): 0 raster; 1 wave groups of gtiles tiles in strips sw tiles wide
   double wc[27];              // weights, lexicographic (dz, dy, dx); centre unused
 };
 
@@ -64,6 +65,40 @@ __device__ __forceinline__ double2 ld_d2_cs(const double* p) {
 }
 __device__ __forceinline__ void st_d2_cs(double* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// Item -> (probe slice, tile, z segment).  Order 0: slice fastest, then x tiles,
+// y tiles, z segments.  Order 1: the tiles are numbered in column strips `sw`
+// tiles wide (a compact patch instead of a few full rows) and cut into groups
+// of `gtiles` (= one wave of the persistent grid); a group runs all its z
+// segments before the next group starts, so the blocks in flight share halos
+// with each other and a segment's first planes were the previous wave's last.
+__device__ __forceinline__ void zm_decode(const ZmArgs& t, int64_t item, int& slice, int& xt, int& yt, int& zs) {
+  slice = (int)(item % t.slices);
+  int64_t sp = item / t.slices;
+  if (t.order == 0) {
+    xt = (int)(sp % t.n_xt);
+    sp /= t.n_xt;
+    yt = (int)(sp % t.n_yt);
+    zs = (int)(sp / t.n_yt);
+    return;
+  }
+  const int ntiles = t.n_xt * t.n_yt;
+  const int64_t per_group = (int64_t)t.gtiles * t.n_zs;
+  const int full = ntiles / t.gtiles;
+  int group = (int)(sp / per_group), tig = t.gtiles;
+  int64_t r = sp - (int64_t)group * per_group;
+  if (group >= full) {
+    group = full;
+    r = sp - (int64_t)full * per_group;
+    tig = ntiles - full * t.gtiles;
+  }
+  zs = (int)(r / tig);
+  const int u = group * t.gtiles + (int)(r % tig);
+  const int per_strip = t.sw * t.n_yt;
+  const int strip = u / per_strip, within = u % per_strip;
+  yt = within / t.sw;
+  xt = strip * t.sw + within % t.sw;
 }
 
 // Which in-plane positions (dy, dx) a shape reads: bit (dy+1)*3 + (dx+1).
@@ -166,12 +201,8 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
       int s = 0;
       uint32_t use = 0;
       for (int64_t item = blockIdx.x; item < t.items; item += G_) {
-        const int slice = (int)(item % t.slices);
-        int64_t sp = item / t.slices;
-        const int xt = (int)(sp % t.n_xt);
-        sp /= t.n_xt;
-        const int yt = (int)(sp % t.n_yt);
-        const int zs = (int)(sp / t.n_yt);
+        int slice, xt, yt, zs;
+        zm_decode(t, item, slice, xt, yt, zs);
         const int zbeg = t.z_lo + zs * t.ZS, zend = min(zbeg + t.ZS, t.z_hi);
         const int c0 = slice * CS, x0 = xt * TX, y0 = yt * TY;
         for (int p = zbeg - 1; p <= zend; ++p) {
@@ -212,12 +243,8 @@ __global__ void __launch_bounds__(ZmGeom<CS, TX, TY, PPT>::NT + 32, 1)
   int pb_row = -1;     // partial row of this block (fixed slice: gridDim % slices == 0)
   int col0 = 0;
   for (int64_t item = blockIdx.x; item < t.items; item += G_) {
-    const int slice = (int)(item % t.slices);
-    int64_t sp = item / t.slices;
-    const int xt = (int)(sp % t.n_xt);
-    sp /= t.n_xt;
-    const int yt = (int)(sp % t.n_yt);
-    const int zs = (int)(sp / t.n_yt);
+    int slice, xt, yt, zs;
+    zm_decode(t, item, slice, xt, yt, zs);
     const int zbeg = t.z_lo + zs * t.ZS, zend = min(zbeg + t.ZS, t.z_hi);
     col0 = slice * CS;
     pb_row = (int)(blockIdx.x / t.slices);
@@ -1006,6 +1033,10 @@ int zm_launch_step(const sdb_matrix* m, const ZmPlan& p, const StepArgs& a, bool
   t.z_lo = p.z_lo;
   t.z_hi = p.z_hi;
   t.diag = m->diag;
+  t.order = zm_env("SDB_ZM_ORDER", 0);
+  t.gtiles = (int)(p.grid / t.slices) > 0 ? (int)(p.grid / t.slices) : 1;
+  t.sw = zm_env("SDB_ZM_SW", 8);
+  if (t.sw < 1 || t.n_xt % t.sw != 0) t.sw = t.n_xt;
   t.hint = zm_env("SDB_ZM_HINT", 2);  // measured: x boxes evict_last 69.4 -> 68.6 us (C2), 2427 -> 2392 us (C5)
   for (int o = 0; o < 27; ++o) t.wc[o] = o < m->nterms ? m->term_w_host[o] : 0.0;
   StepArgs aa = a;

@@ -223,9 +223,9 @@ def test_fused_cgs2_pass_matches_four_pass_schedule(monkeypatch, steps):
 @pytest.mark.parametrize("steps", [5, 40, 100, 300])
 def test_gram_two_pass_reorthogonalisation_matches_three_pass(monkeypatch, steps):
     """The two-pass full reorthogonalisation (projection + Gram column, h = 2 h1 - G h1,
-    one update; default for n >= 16384) against the three-pass CGS2 schedule and the
-    oracle on the same probes.  300 steps runs past the Gram matrix (256 steps) and
-    finishes on the fallback schedule."""
+    one update; default for n >= 16384 and steps <= n / 64) against the three-pass CGS2
+    schedule and the oracle on the same probes; 300 steps is past the fused three-pass
+    kernel's range (the comparison run finishes on the 4-pass fallback)."""
     op = W.anderson_3d(12)
     iv = W.gershgorin_interval(op)
     src = sdb.ProbeVectorSource("gaussian", seed=3, dim=op.dim)

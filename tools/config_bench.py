@@ -131,11 +131,11 @@ def main():
             ma = device_matrix(res.base, dev, E.stream_ptr(dev)).bytes_per_pass
             m = cfg.degree
             # traffic of the schedule that ran.  Two-pass Gram-corrected CGS2 (default for
-            # n >= 16384, <= 256 steps): SpMM 4 block passes + proj (V, w, v_j) + update (V, w rmw);
+            # n >= 16384, steps <= n / 64): SpMM 4 block passes + proj (V, w, v_j) + update (V, w rmw);
             # fused three-pass (SDB_LZ_GRAM=0): SpMM 4 + proj (V, w) + K5c (V, w in, w out) +
             # update (V, w rmw); SDB_LZ_FUSED=0 as well: the 4-pass reference order
             genv = os.environ.get("SDB_LZ_GRAM", "")
-            gram = m <= 256 and (genv == "1" or (genv != "0" and n >= 16384))
+            gram = genv == "1" or (genv != "0" and n >= 16384 and m <= n // 64)
             fused = os.environ.get("SDB_LZ_FUSED", "1") != "0" and m <= 256
             per_step = (lambda j: 2 * (j + 1) + 8) if gram else (
                 (lambda j: 3 * (j + 1) + 9) if fused else (lambda j: 4 * (j + 1) + 11))
