@@ -822,6 +822,34 @@ static int band_moments(const sdb_matrix* m, const StepPlan& P0, const BandPlan&
   return SDB_OK;
 }
 
+// Moment run on the cluster-resident path (resident.cu): every step in one
+// launch, K2 over its per-warp partial rows.  The recurrence blocks of the
+// workspace are not used; the partials sit at its start.
+static int resident_moments(const sdb_matrix* m, const StepPlan& P0, const ResPlan& rp, int64_t n_vec,
+                            int64_t degree, int mode, const double* probes, double* zeta_pp, void* workspace,
+                            cudaStream_t s, float* step_ms) {
+  double* partials = (double*)workspace;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (step_ms) {
+    SDB_CUDA(cudaEventCreate(&e0));
+    SDB_CUDA(cudaEventCreate(&e1));
+    SDB_CUDA(cudaEventRecord(e0, s));
+  }
+  int rc = res_launch(m, rp, P0.a, degree, mode, probes, partials, s);
+  if (rc) return rc;
+  if (step_ms) SDB_CUDA(cudaEventRecord(e1, s));
+  StepPlan P = P0;
+  P.a.nblocks = rp.nblocks;
+  if ((rc = launch_reduce(P, n_vec, degree, mode, partials, zeta_pp, s))) return rc;
+  if (step_ms) {
+    SDB_CUDA(cudaEventSynchronize(e1));
+    SDB_CUDA(cudaEventElapsedTime(step_ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  return SDB_OK;
+}
+
 }  // namespace sdb
 
 using namespace sdb;
@@ -864,6 +892,8 @@ const char* sdb_cheb_kernel(const sdb_matrix* m, int64_t n_vec, int mode) {
   if (band_plan(m, n_vec, mode, &bp) == SDB_OK && bp.on) return "cheb_step_band";
   ZmPlan zp;
   if (zm_plan(m, g.ldv, mode, &zp) == SDB_OK && zp.on) return zp.name;
+  ResPlan rp;
+  if (res_plan(m, n_vec, mode, &rp) == SDB_OK && rp.on) return "cheb_resident";
   if (m->format == SDB_FMT_CSR) return "cheb_step_csr";
   if (plan_tile(m, g.ldv, mode).on) return "cheb_step_tile";
   if (m->shape == SDB_SHAPE_FACE7 || m->shape == SDB_SHAPE_BOX27) return "cheb_step_grid";
@@ -895,6 +925,11 @@ int sdb_cheb_moments(const sdb_matrix* m, double c, double d, int64_t n_vec, int
     if (bp.on && steps_b > 0)
       return band_moments(m, P, bp, n_vec, degree, mode, probes, zeta_pp, workspace, (cudaStream_t)stream,
                           step_ms);
+    ResPlan rp;
+    if ((rc = res_plan(m, n_vec, mode, &rp))) return rc;
+    if (rp.on && steps_b > 0)
+      return resident_moments(m, P, rp, n_vec, degree, mode, probes, zeta_pp, workspace, (cudaStream_t)stream,
+                              step_ms);
   }
   size_t bb, pb;
   cheb_layout(m, P.g.ldv, degree, &bb, &pb);

@@ -99,6 +99,9 @@ struct sdb_matrix {
   uint4* frec = nullptr;      // records, 13 x 16 B each
   int64_t frecs = 0;          // stored records
   int64_t fnnz = 0;           // far entries (without padding)
+  // cluster-resident recurrence (resident.cu): most CSR entries in one row
+  // block when the rows are cut into 16 / 8 equal blocks (-1: not computed)
+  int32_t res_cap[2] = {-1, -1};
 };
 
 namespace sdb {

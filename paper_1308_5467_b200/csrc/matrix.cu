@@ -241,6 +241,16 @@ int sdb_matrix_create_csr(int device, int64_t n, int64_t nnz, const int64_t* ind
   m->format = SDB_FMT_CSR;
   m->n = n;
   m->nnz = nnz;
+  for (int i = 0; i < 2; ++i) {  // row-block entry counts for the cluster-resident path
+    const int64_t CL = i == 0 ? 16 : 8, R = (n + CL - 1) / CL;
+    int32_t cap = 0;
+    for (int64_t r = 0; r < CL; ++r) {
+      const int64_t lo = r * R < n ? r * R : n, hi = (r + 1) * R < n ? (r + 1) * R : n;
+      const int32_t cnt = rp[(size_t)hi] - rp[(size_t)lo];
+      if (cnt > cap) cap = cnt;
+    }
+    m->res_cap[i] = cap;
+  }
   auto cleanup = [&](int code) {
     sdb_matrix_destroy(m);
     return code;

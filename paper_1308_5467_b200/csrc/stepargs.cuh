@@ -137,6 +137,23 @@ int band_plan(const sdb_matrix* m, int64_t n_vec, int mode, BandPlan* p);
 int band_pack(const sdb_matrix* m, const BandPlan& p, const double* probes, int64_t ldv, double* v0b, double* bufA,
               double* bufB, cudaStream_t s);
 int band_launch_step(const sdb_matrix* m, const BandPlan& p, const StepArgs& a, bool first, int mode, cudaStream_t s);
+// ---- cluster-resident recurrence for small CSR matrices (resident.cu) ---------------
+// The whole recurrence in one launch: clusters of CL CTAs own column groups,
+// each CTA keeps its rows of w_k / w_{k-1} and its CSR slice in shared memory.
+struct ResPlan {
+  bool on = false;
+  int CL = 0;              // CTAs per cluster (row blocks)
+  int lpr = 0;             // lanes per row: 2 * lpr probe columns per cluster
+  int R = 0;               // rows per CTA
+  int nnz_cap = 0;         // CSR entries staged per CTA
+  int64_t clusters = 0;
+  int64_t nblocks = 0;     // partial rows (CL * warps per CTA)
+  size_t smem = 0;
+};
+int res_plan(const sdb_matrix* m, int64_t n_vec, int mode, ResPlan* p);
+// all steps of the moment run; partials [(degree+1)][p.nblocks][ldv]
+int res_launch(const sdb_matrix* m, const ResPlan& p, const StepArgs& a, int64_t degree, int mode,
+               const double* probes, double* partials, cudaStream_t s);
 // probes (n x ldv) -> padded block
 int zm_pad(const sdb_matrix* m, const ZmPlan& p, const double* probes, int64_t ldv, double* padded, cudaStream_t s);
 
