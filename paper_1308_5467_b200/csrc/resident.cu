@@ -65,6 +65,12 @@ __device__ __forceinline__ uint32_t res_cluster_size() {
 __device__ __forceinline__ void res_cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void res_cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void res_cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void res_cluster_sync_diag(int diag) {
   if (diag & 4) {
     __syncthreads();
@@ -241,6 +247,12 @@ __global__ void __launch_bounds__(kResThreads, 1) cheb_resident(ResArgs a) {
       finish(r0, y0);
       if (ok1) finish(r1, y1);
     }
+    // w_{k+1} complete everywhere, every remote read of w_k retired: arrive now,
+    // sum the step's dots (registers only) while the other CTAs arrive, then wait
+    if (a.diag)
+      res_cluster_sync_diag(a.diag);
+    else
+      res_cluster_arrive();
     accA = res_warp_sum<LPR>(accA);
     if (MODE == SDB_CHEB_DOUBLING) accB = res_warp_sum<LPR>(accB);
     if (k == 0) store_partial(res_warp_sum<LPR>(accZ), 0);
@@ -252,11 +264,7 @@ __global__ void __launch_bounds__(kResThreads, 1) cheb_resident(ResArgs a) {
     } else {
       pslotA = k + 1;
     }
-    // w_{k+1} complete everywhere, every remote read of w_k retired
-    if (a.diag)
-      res_cluster_sync_diag(a.diag);
-    else
-      res_cluster_sync();
+    if (!a.diag) res_cluster_wait();
     const uint32_t t = cur_s;
     cur_s = oth_s;
     oth_s = t;

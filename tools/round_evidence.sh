@@ -10,6 +10,7 @@ python bench.py --gpus 1 --steps 20 --warmup 5 > $O/${TAG}_bench_c3.json 2> $O/$
 python bench.py --impl reference --gpus 1 --steps 20 --warmup 5 > $O/${TAG}_bench_reference_c3.json 2>> $O/${TAG}_bench_c3.err
 python bench.py --config C2 --steps 20 --warmup 5 > $O/${TAG}_bench_c2.json 2>> $O/${TAG}_bench_c3.err
 python bench.py --config C5 --steps 3 --warmup 3 > $O/${TAG}_bench_c5.json 2>> $O/${TAG}_bench_c3.err
+python bench.py --config C1 --steps 50 --warmup 10 > $O/${TAG}_bench_c1.json 2>> $O/${TAG}_bench_c3.err
 # every config with its CPU baseline beside it
 python tools/config_bench.py C1 C2 C3 C4 C5 --cpu > $O/${TAG}_configs.jsonl 2> $O/${TAG}_configs.err
 # launch list of the bench command (after it exited 0 without ncu, above)
@@ -31,4 +32,5 @@ ncu --set full --clock-control none -k regex:cheb_step_zmarch -s 3 -c 1 -o $O/${
 python tools/ncu_summary.py $O/${TAG}_zmarch_c5.ncu-rep > $O/${TAG}_ncu_zmarch_c5.txt 2>&1
 # the reference's own test modules against the drop-in
 python -m pytest tests/test_reference_suite.py -m gpu -q -rA 2>&1 | tail -15 > $O/${TAG}_reference_suite.txt
+python -c "import __graft_entry__ as g; g.smoke()" > $O/${TAG}_smoke.txt 2>&1
 ls -la $O | tail -30
