@@ -149,6 +149,7 @@ def kernel_label(dm, n_vec, mode):
               "cheb_step_tile": "2.5-D cp.async shared-memory tiles",
               "cheb_step_grid": "row panels", "cheb_step_csr": "CSR row groups",
               "cheb_step_stencil": "generic stencil",
+              "cheb_resident": "cluster-resident: all steps in one launch, rows in distributed shared memory",
               "cheb_step_band": "probe-sliced symmetric band (DIA, shared-memory window) + SELL-4 far gathers "
                                 "from an L2-resident probe slice"}.get(name, "")
     return f"{name} ({detail})" if detail else name
@@ -466,6 +467,11 @@ def main():
         bytes_launch = dm.bytes_per_pass + 32 * n * count
         launches = pairs + singles
         total_bytes = pairs * bytes_launch + singles * one_step_bytes
+    elif kname == "cheb_resident":
+        # cluster-resident path: every recurrence step of the estimate in ONE launch
+        launches = 1
+        bytes_launch = steps_per_probe * one_step_bytes
+        total_bytes = bytes_launch
     else:
         bytes_launch = one_step_bytes
         launches = steps_per_probe
