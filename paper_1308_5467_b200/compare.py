@@ -46,11 +46,15 @@ def kpm_dos_device(mapped, degree, source, n_vec, damping, grid, product_formula
     """Moments -> DOS entirely on device.  Returns (zeta, values, density, run)."""
     torch = E._torch()
     mode = _native.SDB_CHEB_DOUBLING if product_formula else _native.SDB_CHEB_DIRECT
+    # the grid goes up first: its (synchronous, pageable) copy would otherwise make the host wait for
+    # the moment run before it can queue the evaluation kernels behind it
+    primary = E.require_cuda(device)
+    with torch.cuda.device(primary):
+        t_dev = E.to_device(grid, primary)
     run = E.run_chebyshev(mapped, degree, source, n_vec, mode, device=device, probes=probes, time_steps=time_steps)
     dev = run.zeta_pp.device
     with torch.cuda.device(dev):
         zeta_dev, flag = E.mean_moments(run.zeta_pp, dev)
-        t_dev = E.to_device(grid, dev)
         damp = _native.SDB_DAMP_JACKSON if damping == "jackson" else _native.SDB_DAMP_NONE
         _, values, density = E.kpm_density_device(zeta_dev, degree, run.n, damp, t_dev, run.resolved.d, dev)
         packed = torch.cat([zeta_dev, values, density, flag.to(torch.float64)]).cpu().numpy()
