@@ -14,6 +14,7 @@ them is unobservable, and repeated estimates over the same probes then cost
 one host->device copy instead of a re-draw.
 """
 
+import os
 import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
@@ -91,7 +92,7 @@ class ProbeVectorSource:
             arr[i] = np.packbits(rng.integers(0, 2, self.dim).astype(np.uint8), bitorder="little")
 
         if count >= 4:
-            with ThreadPoolExecutor(max_workers=min(8, count)) as ex:
+            with ThreadPoolExecutor(max_workers=min(_DRAW_THREADS, count)) as ex:
                 list(ex.map(one, range(count)))
         else:
             for i in range(count):
@@ -108,6 +109,8 @@ class ProbeVectorSource:
 
 
 _pool_lock = threading.Lock()
+# host threads that draw probe rows in parallel (NumPy's generators release the GIL)
+_DRAW_THREADS = max(1, min(32, os.cpu_count() or 8))
 
 
 def _draw_rows(source, start, count, out):
@@ -116,7 +119,7 @@ def _draw_rows(source, start, count, out):
 
     if count >= 4:
         # drawing is NumPy C code that releases the GIL; fill rows in parallel
-        with ThreadPoolExecutor(max_workers=min(8, count)) as ex:
+        with ThreadPoolExecutor(max_workers=min(_DRAW_THREADS, count)) as ex:
             list(ex.map(one, range(count)))
     else:
         for i in range(count):
