@@ -16,8 +16,8 @@ def main():
     from paper_1308_5467_b200 import workloads as W
 
     degree = int(sys.argv[1]) if len(sys.argv) > 1 else 100
-    variants = sys.argv[2:] or ["", "SDB_BAND_DIAG=1", "SDB_BAND_DIAG=2", "SDB_BAND_DIAG=4", "SDB_BAND_DIAG=5",
-                                "SDB_BAND_PERSLICE=1", "SDB_BAND_BPS=1", "SDB_BAND_S=8", "SDB_BAND=0"]
+    variants = sys.argv[2:] or ["", "SDB_BAND_DIAG=4", "SDB_BAND_DIAG=8", "SDB_BAND_DIAG=12", "SDB_BAND_DIAG=16",
+                                "SDB_BAND_NB=2", "SDB_BAND=0"]
     cfg = W.CONFIGS["C3"]
     op = W.build_matrix("C3")
     iv = W.gershgorin_interval(op)
